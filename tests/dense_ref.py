@@ -1,0 +1,132 @@
+"""Dense brute-force reference of one ADI step, straight from the weak forms.
+
+Test code (pin P2 of SURVEY.md §8(c)).  It shares nothing with ``oracle/``:
+the 1D basis comes from ``scipy.interpolate.BSpline`` and the Gauss rule from
+``numpy.polynomial.legendre``; the 3D matrices are assembled by 3D quadrature
+of the integrands printed in PAPER.md ``weak1``-``weak4`` -- no 1D
+matrices and no Kronecker factoring of the operators -- then row-scaled by
+the material of each test function (D5), restricted to the PEC active set
+(D1) and solved densely with ``numpy.linalg.solve``.
+
+Only tiny grids (<= 5^3 elements) are meant to go through here.
+"""
+from __future__ import annotations
+
+import numpy as np
+from numpy.polynomial.legendre import leggauss
+from scipy.interpolate import BSpline
+
+
+class DenseMaxwell:
+    def __init__(self, n: int, p: int, tau: float, pec: bool = True):
+        self.n, self.p, self.tau, self.pec = n, p, tau, pec
+        N = n + p
+        self.N, self.U = N, N ** 3
+        t = np.concatenate([np.zeros(p + 1), np.arange(1, n) / n, np.ones(p + 1)])
+        q = p + 1  # exact for every integrand below (degree <= 2p per axis)
+        gx, gw = leggauss(q)
+        pts, wts = [], []
+        for e in range(n):
+            a, b = e / n, (e + 1) / n
+            pts.append(a + (gx + 1) * (b - a) / 2)
+            wts.append(gw * (b - a) / 2)
+        x = np.concatenate(pts)
+        w = np.concatenate(wts)
+        spl = BSpline(t, np.eye(N), p, extrapolate=False)
+        Bv = np.nan_to_num(spl(x))  # (nq, N)
+        Bd = np.nan_to_num(spl.derivative(1)(x))
+        # 3D basis at the 3D Gauss points: Phi[P, I] = B_i(x_P) B_j(y_P) B_k(z_P)
+        # with I = i + N j + N^2 k and P = px + nq py + nq^2 pz (x fastest).
+        K = lambda bz, by, bx: np.kron(np.kron(bz, by), bx)
+        self.Phi = K(Bv, Bv, Bv)
+        self.D = [K(Bv, Bv, Bd), K(Bv, Bd, Bv), K(Bd, Bv, Bv)]  # d/dx1, d/dx2, d/dx3
+        self.W = np.kron(np.kron(w, w), w)
+
+    # (f, g) with f = trial operator, g = test operator: rows = test functions
+    def form(self, test, trial):
+        return test.T @ (self.W[:, None] * trial)
+
+    def active(self, comp: int) -> np.ndarray:
+        """Boolean mask of active coefficients (D1)."""
+        N = self.N
+        i, j, k = np.meshgrid(np.arange(N), np.arange(N), np.arange(N), indexing="ij")
+        ijk = [i, j, k]
+        m = np.ones((N, N, N), dtype=bool)
+        if self.pec and comp < 3:
+            for ax in range(3):
+                if ax != comp:
+                    m &= (ijk[ax] >= 1) & (ijk[ax] <= N - 2)
+        # back to x-fastest flat order
+        return m.transpose(2, 1, 0).reshape(-1)
+
+    def step(self, E, H, a, b, c, s_val=0.0, J=None):
+        """One full step (weak1 -> weak2 -> weak3 -> weak4).
+
+        E, H: lists of 3 flat arrays; a, b, c: per-test-function row factors
+        tau/(2 eps), tau/(2 mu), tau^2/(4 eps mu); J: list of 3 load vectors
+        or None; s_val the signal value of this step (D9).
+        """
+        Phi, D = self.Phi, self.D
+        Mass = self.form(Phi, Phi)
+        # (d_a trial, V)
+        Adv = [self.form(Phi, D[ax]) for ax in range(3)]
+        # (d_a trial, d_b test)
+        Mix = lambda ta, tb: self.form(D[tb], D[ta])
+        Stf = [Mix(ax, ax) for ax in range(3)]
+        E = [np.asarray(e, dtype=float).copy() for e in E]
+        H = [np.asarray(h, dtype=float).copy() for h in H]
+        for d in range(3):
+            E[d][~self.active(d)] = 0.0
+
+        def solve_E(lhs_stiff_axis, d, rhs):
+            act = self.active(d)
+            L = Mass + c[:, None] * Stf[lhs_stiff_axis]
+            x = np.zeros(self.U)
+            x[act] = np.linalg.solve(L[np.ix_(act, act)], rhs[act])
+            return x
+
+        def source(d):
+            if J is None or J[d] is None:
+                return 0.0
+            return -a * s_val * J[d]
+
+        # ---- weak1: substep-1 E systems -------------------------
+        # LHS: (E1,V1)+c(d2 E1, d2 V1); (E2,V2)+c(d3 E2,d3 V2); (E3,V3)+c(d1 E3,d1 V3)
+        # RHS: (E^n,V) + a[(-d3 H2 + d2 H3, V1) + (d3 H1 - d1 H3, V2) + (-d2 H1 + d1 H2, V3)]
+        #      + c[(d1 E2, d2 V1) + (d2 E3, d3 V2) + (d3 E1, d1 V3)]
+        R = [
+            Mass @ E[0] + a * (-Adv[2] @ H[1] + Adv[1] @ H[2]) + c * (Mix(0, 1) @ E[1]) + source(0),
+            Mass @ E[1] + a * (Adv[2] @ H[0] - Adv[0] @ H[2]) + c * (Mix(1, 2) @ E[2]) + source(1),
+            Mass @ E[2] + a * (-Adv[1] @ H[0] + Adv[0] @ H[1]) + c * (Mix(2, 0) @ E[0]) + source(2),
+        ]
+        Eh = [solve_E(1, 0, R[0]), solve_E(2, 1, R[1]), solve_E(0, 2, R[2])]
+        # ---- weak2: substep-1 H systems -------------------------
+        # (H^{1/2},V) = (H^n,V) - b[(d2 E3^n,V1)+(d3 E1^n,V2)+(d1 E2^n,V3)]
+        #                      + b[(d3 E2^h,V1)+(d1 E3^h,V2)+(d2 E1^h,V3)]
+        Mi = np.linalg.inv(Mass)
+        G = [
+            Mass @ H[0] - b * (Adv[1] @ E[2]) + b * (Adv[2] @ Eh[1]),
+            Mass @ H[1] - b * (Adv[2] @ E[0]) + b * (Adv[0] @ Eh[2]),
+            Mass @ H[2] - b * (Adv[0] @ E[1]) + b * (Adv[1] @ Eh[0]),
+        ]
+        Hh = [np.linalg.solve(Mass, g) for g in G]
+        del Mi
+        # ---- weak3: substep-2 E systems -------------------------
+        # LHS: (E1,V1)+c(d3 E1,d3 V1); (E2,V2)+c(d1 E2,d1 V2); (E3,V3)+c(d2 E3,d2 V3)
+        # RHS: (E^h,V) + a[C-term with H^h] + c[(d1 E3,d3 V1)+(d2 E1,d1 V2)+(d3 E2,d2 V3)]
+        R = [
+            Mass @ Eh[0] + a * (-Adv[2] @ Hh[1] + Adv[1] @ Hh[2]) + c * (Mix(0, 2) @ Eh[2]) + source(0),
+            Mass @ Eh[1] + a * (Adv[2] @ Hh[0] - Adv[0] @ Hh[2]) + c * (Mix(1, 0) @ Eh[0]) + source(1),
+            Mass @ Eh[2] + a * (-Adv[1] @ Hh[0] + Adv[0] @ Hh[1]) + c * (Mix(2, 1) @ Eh[1]) + source(2),
+        ]
+        E1 = [solve_E(2, 0, R[0]), solve_E(0, 1, R[1]), solve_E(1, 2, R[2])]
+        # ---- weak4: substep-2 H systems -------------------------
+        # (H^{n+1},V) = (H^h,V) + b[(d3 E2^h,V1)+(d1 E3^h,V2)+(d2 E1^h,V3)]
+        #                       - b[(d2 E3^{n+1},V1)+(d3 E1^{n+1},V2)+(d1 E2^{n+1},V3)]
+        G = [
+            Mass @ Hh[0] + b * (Adv[2] @ Eh[1]) - b * (Adv[1] @ E1[2]),
+            Mass @ Hh[1] + b * (Adv[0] @ Eh[2]) - b * (Adv[2] @ E1[0]),
+            Mass @ Hh[2] + b * (Adv[1] @ Eh[0]) - b * (Adv[0] @ E1[1]),
+        ]
+        H1 = [np.linalg.solve(Mass, g) for g in G]
+        return E1, H1
