@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the ADI-IGA Maxwell time step (arXiv 2103.06998) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Metric (BASELINE.json): field DOF-updates/s per
+time step (fp64) and the HBM roofline fraction of the dominant kernel class.
+
+Workload: BASELINE config c5 (512^3 elements, p=2, seeded ellipsoid phantom with
+per-voxel eps_r ~ U[1,80], mu_r=1, tau=1e-2) -- the configuration the metric's
+"1/2/4/8 B200" is quoted on; it fits one B200 (~23 GB).  Inputs: seeded
+synthetic (workloads/), every field 1.09 GB >> 126 MB L2 (no L2 flush needed).
+
+Timed region: W untimed warm-up steps, then EXACTLY K steps bracketed by
+barrier + cudaDeviceSynchronize, timed with CUDA events on the library's
+stream; each kernel launch is bracketed by CUDA events on the same stream
+(adi_set_timing) for the per-kernel roofline.  nvidia-smi clocks are sampled
+during the timed region.
+
+--impl reference runs the CPU oracle (oracle/, plain C, one core) on a bounded
+sample of the same workload (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+METRIC = "field DOF-updates/sec per time step (fp64) at 1/2/4/8 B200 and % of HBM roofline"
+UNIT = "DOF-updates/s"
+FALLBACK_HBM = 6650.0
+
+
+def dof_count(n: int, p: int) -> int:
+    """Free coefficients of the six fields under PEC (D1): 3 N (N-2)^2 + 3 N^3."""
+    N = n + p
+    return 3 * N * (N - 2) ** 2 + 3 * N ** 3
+
+
+def algorithmic_bytes(n: int, p: int):
+    """Algorithmic HBM bytes per launch of each kernel class.
+
+    Units: U = N^3 coefficients; Ue = N (N-2)^2 active rows of an E component.
+      rhs_e      : 11 U * 8 B per substep (read E,H,a,c; write R), 3 launches/substep
+      rhs_h      : 13 U * 8 B per substep (read H,E^old,E^new,b; write G), 3 launches
+      sweep_mass : 16 B per active row (read rhs, write solution)
+      sweep_mod  : 24 B per active row (read rhs and c, write solution)
+    Per step: 12 mass sweeps on E sets + 18 on H sets; 6 row-modified sweeps on E sets.
+    """
+    N = n + p
+    U = N ** 3
+    Ue = N * (N - 2) ** 2
+    return {
+        "rhs_e": 11 * U * 8 / 3.0,
+        "rhs_h": 13 * U * 8 / 3.0,
+        "sweep_mass": 16.0 * (12 * Ue + 18 * U) / 30.0,
+        "sweep_mod": 24.0 * Ue,
+    }
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = f"/tmp/adi_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        # median over the samples taken under load (top half of the clock samples)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_inputs(cfg, seed=12345, pinned=False):
+    import torch
+
+    n, p = cfg["n"], cfg["p"]
+    N = n + p
+    eps = workloads.element_eps(n, cfg["material"])
+    # seeded random coefficient fields, generated in chunks into (pinned) host tensors
+    rng = np.random.default_rng(seed)
+    U = N ** 3
+    fields = []
+    for _ in range(6):
+        t = torch.empty(U, dtype=torch.float64, pin_memory=pinned)
+        a = t.numpy()
+        step = 1 << 24
+        for o in range(0, U, step):
+            a[o:o + step] = rng.uniform(-1.0, 1.0, size=min(step, U - o))
+        fields.append(t)
+    return eps, fields
+
+
+def cpu_oracle_rate(cfg, steps: int, sample_n: int):
+    """The oracle as it stands (oracle/, one core) on a bounded sample of the workload:
+    the same recipe at n = sample_n.  Returns (DOF-updates/s, seconds, description)."""
+    import oracle
+
+    n, p = sample_n, cfg["p"]
+    N = n + p
+    P = oracle.Patch(n, p, cfg["tau"])
+    P.set_materials(workloads.element_eps(n, cfg["material"]))
+    P.set_fields(workloads.random_fields(N, 1))
+    t0 = time.perf_counter()
+    P.step(steps)
+    dt = time.perf_counter() - t0
+    rate = dof_count(n, p) * steps / dt
+    desc = (f"{cfg['name']} recipe at n={n} (N={N}, {dof_count(n, p)} DOF), {steps} step(s), "
+            f"single-threaded C oracle, setup excluded")
+    return rate, dt, desc
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        backend = "nccl"
+        dist.init_process_group(backend=backend)
+        return dist, dist.get_rank(), ws
+    return None, 0, 1
+
+
+def run_reference(args, cfg):
+    dist, rank, ws = dist_init()
+    if rank != 0:
+        return
+    sample_n = args.oracle_n
+    rates = []
+    # warm-up steps are untimed; then K timed oracle steps of the bounded sample
+    import oracle
+
+    n, p = sample_n, cfg["p"]
+    N = n + p
+    P = oracle.Patch(n, p, cfg["tau"])
+    P.set_materials(workloads.element_eps(n, cfg["material"]))
+    P.set_fields(workloads.random_fields(N, 1))
+    P.step(args.warmup)
+    t0 = time.perf_counter()
+    P.step(args.steps)
+    dt = time.perf_counter() - t0
+    rate = dof_count(n, p) * args.steps / dt
+    desc = (f"{cfg['name']} recipe at n={n} (N={N}), {args.steps} timed steps after {args.warmup} warm-up, "
+            f"single-threaded C oracle")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(cfg, args),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def config_dict(cfg, args):
+    n, p = cfg["n"], cfg["p"]
+    return {
+        "workload": (f"{cfg['name']}: {n}^3 elements, p={p} (C^{p - 1}), N={n + p}, PEC, tau={cfg['tau']}, "
+                     f"material={cfg['material']}, seeded random fields"),
+        "n": n, "p": p, "N": n + p, "tau": cfg["tau"], "dof_per_step": dof_count(n, p),
+        "l2_policy": "inputs larger than L2 (each field %.2f GB > 126 MB)" % ((n + p) ** 3 * 8 / 1e9),
+        "parallelism": ("single GPU" if args.gpus == 1 else
+                        f"{args.gpus} independent replicas (slab decomposition not yet implemented)"),
+    }
+
+
+def run_ours(args, cfg):
+    import torch
+
+    dist, rank, ws = dist_init()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    import paper_2103_06998_b200 as adi
+
+    adi.build()
+    n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
+    N = n + p
+    U = N ** 3
+    eps, fields = make_inputs(cfg, seed=1000 + rank, pinned=True)
+    G = adi.Patch(n, p, tau, device=local)
+    G.set_materials(eps)
+    del eps
+    G.set_fields(fields)
+    G.step(args.warmup)
+    G.synchronize()
+    # ---------------- timed region (device-resident state) ----------------
+    G.set_timing(True)
+    stream = torch.cuda.ExternalStream(G.stream, device=local)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        G.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    rep = G.timing_report()
+    G.set_timing(False)
+    clocks = clk.summary()
+    # ---------------- end-to-end through the public API, host buffers ---------
+    out_host = [torch.empty(U, dtype=torch.float64, pin_memory=True) for _ in range(6)]
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    G.set_fields(fields)  # pinned host -> device (synchronous)
+    G.step(args.steps)    # graph path
+    G.get_fields(out_host)  # device -> pinned host (synchronises)
+    e2e_s = time.perf_counter() - t0
+    h2d = 6 * U * 8 / args.steps
+    d2h = 6 * U * 8 / args.steps
+    launches = args.steps * G.launches_per_step
+    ms_t = torch.tensor([ms, e2e_s * 1e3], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(ms_t[0]), float(ms_t[1])
+    if rank != 0:
+        G.close()
+        return
+    dofs = dof_count(n, p)
+    value = ws * dofs * args.steps / (ms * 1e-3)
+    e2e_value = ws * dofs * args.steps / (e2e_ms * 1e-3)
+    # roofline of the dominant kernel class
+    peak, peak_src = hbm_peak()
+    algo = algorithmic_bytes(n, p)
+    cls = max(algo, key=lambda k: rep[k][0])
+    t_cls, n_cls = rep[cls]
+    achieved = algo[cls] / (t_cls * 1e-3 / n_cls) / 1e9
+    traffic = None
+    try:
+        with open(TRAFFIC_PATH) as f:
+            tr = json.load(f)
+        if tr.get("config") == cfg["name"] and cls in tr.get("bytes_per_launch", {}):
+            traffic = tr["bytes_per_launch"][cls]
+    except Exception:
+        pass
+    kernels = {}
+    for k, (t, cnt) in rep.items():
+        if cnt == 0:
+            continue
+        kd = {"ms_total": t, "launches": cnt, "share": t / sum(v[0] for v in rep.values())}
+        if k in algo:
+            kd["achieved_gbs"] = algo[k] / (t * 1e-3 / cnt) / 1e9
+            kd["frac"] = kd["achieved_gbs"] / peak
+        kernels[k] = kd
+    # end-to-end HBM fraction of the step (reference schedule, 168 B / DOF)
+    step_bytes = 126 * U * 8
+    cpu = None
+    if not args.no_cpu_baseline:
+        rate, dt, desc = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, args),
+        "roofline": {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": algo[cls]},
+        "step_hbm_frac": (step_bytes / (ms * 1e-3 / args.steps) / 1e9) / peak,
+        "kernels": kernels,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms": e2e_ms, "note": "set_fields(pinned host) + step(K) via CUDA graph + get_fields(pinned host)"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    G.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--oracle-n", type=int, default=48, help="n of the bounded CPU-oracle sample")
+    ap.add_argument("--oracle-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(workloads.CONFIGS[args.config])
+    cfg["name"] = args.config
+    if args.warmup < 3:
+        print("warning: warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * adi_maxwell.h -- C ABI of libadimaxwell.so, the B200 (sm_100a) hot path of
+ * the alternating-direction-implicit isogeometric Maxwell solver of
+ * arXiv 2103.06998 (Paszynski, Los, Munoz-Matute).  PAPER.md line numbers are
+ * cited as P:<line>; readings of silent/garbled passages as D1..D16
+ * (restated in DESIGN.md).
+ *
+ * What one call of adi_step(k) computes, per time step n -> n+1 (two
+ * substeps, P:95-121 scheme1a-scheme1d; discrete form P:233-258
+ * discrete1-discrete4):
+ *   substep 1: R = M E^n + (tau/2eps) C H^n + (tau^2/4eps mu) R1 E^n      (discrete1)
+ *              (M + tau^2/(4 eps mu) K1) E^{n+1/2} = R                    -> 3 sweeps per component
+ *              M H^{n+1/2} = M H^n - (tau/2mu) C1 E^n + (tau/2mu) C2 E^{n+1/2}   (discrete2)
+ *   substep 2: same with K2, R2 and (discrete4, sign per D2)
+ * with per-test-function material (D5): row rst of every system
+ * uses a = tau/(2 eps^_rst), b = tau/(2 mu^_rst), c = tau^2/(4 eps^ mu^)_rst,
+ * and the stiffened (row-modified) sweep is solved first (D7).
+ * PEC by elimination (D1): E_d drops the first and last B-spline along every
+ * axis a != d; those coefficients are held at 0.
+ *
+ * Layout (D14): every field is N^3 doubles, N = n + p, coefficient (i,j,k)
+ * at i + N*(j + N*k) (x fastest).  Element (a,b,c) at a + n*(b + n*c).
+ * Components: f[0..2] = E1,E2,E3 ; f[3..5] = H1,H2,H3.
+ *
+ * Pointers: every `const double*` / `double*` argument may be a host pointer
+ * or a CUDA device pointer of the patch's device (classified with
+ * cudaPointerGetAttributes); copies run on the patch stream.  The caller owns
+ * all pointers; the library copies on set_* and never keeps caller pointers
+ * beyond the call.  The patch owns its device buffers (cudaMalloc).
+ *
+ * Errors: every call returns adi_status; no C++ exception crosses the ABI.
+ * ADI_ERR_CUDA / ADI_ERR_NCCL poison the patch: every later call except
+ * adi_destroy returns the same code.  A failed set_* leaves the previous
+ * state intact.  adi_last_error() returns a thread-local message valid until
+ * the next call on the same thread.
+ *
+ * Threading: a patch is not thread-safe; separate patches are independent.
+ */
+#ifndef ADI_MAXWELL_H
+#define ADI_MAXWELL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct adi_patch_s* adi_patch; /* opaque; owns device state */
+
+typedef enum {
+  ADI_OK = 0,
+  ADI_ERR_ARG = 1,      /* invalid argument (message names the first offending index) */
+  ADI_ERR_STATE = 2,    /* e.g. adi_step before adi_set_fields */
+  ADI_ERR_SINGULAR = 3, /* a pivot |u_kk| < 1e-14 max|row| in a factorisation */
+  ADI_ERR_CUDA = 4,     /* CUDA runtime error: patch poisoned */
+  ADI_ERR_NCCL = 5,     /* reserved for the distributed path: patch poisoned */
+  ADI_ERR_OOM = 6       /* device allocation failed */
+} adi_status;
+
+typedef enum { ADI_BC_PEC = 0, ADI_BC_NATURAL = 1 } adi_bc;
+
+typedef struct {
+  int32_t n;       /* elements per axis, >= 1 (uniform knots on [0,1], open, C^{p-1}) */
+  int32_t p;       /* B-spline degree, 1..5 */
+  double tau;      /* time step, finite, > 0 */
+  int32_t bc;      /* adi_bc; ADI_BC_PEC (D1) is the paper's Eq. (1) E x n = 0 */
+  int32_t device;  /* CUDA device ordinal */
+  int32_t rank;    /* 0 (single GPU; distributed path reserved) */
+  int32_t nranks;  /* 1 */
+  void* stream;    /* cudaStream_t to run on; NULL = a library-owned non-blocking stream */
+} adi_config;
+
+/* Create a patch: assembles the 1D Galerkin matrices M, S, A (B = A^T) by
+ * Gauss quadrature q = p+1 (D4, D11), factors the constant mass sweeps,
+ * allocates 14 N^3 device arrays + sweep scratch, sets eps = mu = 1.
+ * ADI_ERR_ARG: n < 1, p outside 1..5, tau <= 0 / non-finite, bc invalid,
+ * nranks != 1.  ADI_ERR_OOM: device allocation failed.  *out = NULL on error. */
+adi_status adi_create(const adi_config* cfg, adi_patch* out);
+
+/* Free all device state. NULL-safe. */
+void adi_destroy(adi_patch patch);
+
+/* N = n + p and the z-slab [k0, k1) held by this patch (the whole grid: 0, N). */
+adi_status adi_layout(adi_patch patch, int64_t* N, int64_t* k0, int64_t* k1);
+
+/* Change tau; rebuilds the row factors a, b, c (P:545 with tau^ = tau, D13). */
+adi_status adi_set_tau(adi_patch patch, double tau);
+
+/* Element-wise materials eps_elem, mu_elem (n^3 each; mu NULL => 1).  Mapped to
+ * test functions by the B-spline-weighted average (D6):
+ *   eps^_rst = sum_abc w_ra w_sb w_tc eps_abc,  w_ra = int_{elem a} B_r / int B_r.
+ * ADI_ERR_ARG if any value is <= 0 or non-finite (eps, mu >= delta > 0). */
+adi_status adi_set_materials(adi_patch patch, const double* eps_elem, const double* mu_elem);
+
+/* Per-test-function materials given directly (N^3 each; mu NULL => 1). */
+adi_status adi_set_materials_tf(adi_patch patch, const double* eps_tf, const double* mu_tf);
+
+/* Set the six coefficient fields (N^3 each).  PEC-eliminated E entries are
+ * forced to 0 (D1).  Resets nothing else (step index is kept). */
+adi_status adi_set_fields(adi_patch patch, const double* const f[6]);
+
+/* Read the six fields into caller buffers (N^3 each; NULL entries skipped).
+ * Synchronises the patch stream. */
+adi_status adi_get_fields(adi_patch patch, double* const f[6]);
+
+/* Sources (D9): in both substeps of step m, R_d -= a (.) signal[m] * load[d],
+ * load[d] an N^3 load vector (int j_d B_rst) or NULL; signal[m] = s((m+1/2) tau),
+ * 0 past nsig.  load == NULL or nsig == 0 removes the source. */
+adi_status adi_set_source(adi_patch patch, const double* const load[3], const double* signal, int64_t nsig);
+
+/* Point dipole j = e_comp delta(x - x_s) s(t): the library evaluates
+ * load_rst = B_r(xs) B_s(ys) B_t(zs) itself.  comp in 0..2, x_s in [0,1]^3. */
+adi_status adi_set_point_source(adi_patch patch, int32_t comp, double xs, double ys, double zs,
+                                const double* signal, int64_t nsig);
+
+/* Advance k >= 0 full time steps.  Asynchronous on the patch stream (the first
+ * call for a given patch state captures the step into a CUDA graph).
+ * ADI_ERR_STATE before adi_set_fields. */
+adi_status adi_step(adi_patch patch, int64_t k);
+
+/* Block until all work queued on the patch stream has finished. */
+adi_status adi_synchronize(adi_patch patch);
+
+/* Number of full steps taken since creation. */
+int64_t adi_step_index(adi_patch patch);
+
+/* Number of kernel launches one adi_step(1) issues. */
+int64_t adi_launches_per_step(adi_patch patch);
+
+/* The cudaStream_t the patch runs on. */
+void* adi_stream(adi_patch patch);
+
+/* Thread-local message describing the last error (or ""). */
+const char* adi_last_error(void);
+
+/* ---- per-kernel timing (bench instrumentation) -------------------------- */
+/* Kernel classes used by the timing report. */
+enum { ADI_K_RHS_E = 0, ADI_K_RHS_H = 1, ADI_K_SWEEP_MASS = 2, ADI_K_SWEEP_MOD = 3, ADI_K_OTHER = 4, ADI_K_NCLASS = 5 };
+
+/* enable != 0: subsequent adi_step calls launch kernels directly (no graph),
+ * bracketing each launch with CUDA events on the patch stream; accumulated
+ * per-class device time can then be read with adi_timing_report (which
+ * synchronises).  enable == 0 resets and disables. */
+adi_status adi_set_timing(adi_patch patch, int32_t enable);
+adi_status adi_timing_report(adi_patch patch, double ms[ADI_K_NCLASS], int64_t launches[ADI_K_NCLASS]);
+
+/* ---- test-only entry points (per-stage parity) --------------------------- */
+/* Host copies of the dense 1D matrices (N x N each, row = test function). */
+adi_status adi_debug_matrices(adi_patch patch, double* M, double* S, double* A);
+/* Per-test-function eps^, mu^ currently in use (N^3 each). */
+adi_status adi_debug_materials_tf(adi_patch patch, double* eps_tf, double* mu_tf);
+/* One sweep along `axis` for component comp (0..5 selects the PEC active set);
+ * modified != 0 uses M + diag(c) S with the patch's per-row c, else M. */
+adi_status adi_debug_sweep(adi_patch patch, int32_t comp, int32_t axis, int32_t modified, const double* rhs, double* out);
+/* RHS of the E systems of substep s (1|2) from the current fields. */
+adi_status adi_debug_rhs_e(adi_patch patch, int32_t s, double* const R[3]);
+/* RHS of the H systems of substep s given Eo (start of substep) and En. */
+adi_status adi_debug_rhs_h(adi_patch patch, int32_t s, const double* const Eo[3], const double* const En[3], double* const G[3]);
+/* E-component solve of substep s: stiffened sweep first, then the two mass sweeps. */
+adi_status adi_debug_solve_e(adi_patch patch, int32_t s, int32_t d, const double* rhs, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADI_MAXWELL_H */

@@ -1,0 +1,260 @@
+"""B200-native ADI isogeometric Maxwell time stepper (arXiv 2103.06998).
+
+Thin ctypes binding over ``libadimaxwell.so`` (C ABI in ``include/adi_maxwell.h``):
+argument marshalling only -- every step of the hot path runs in the library's
+sm_100a CUDA kernels.  There is no CPU fallback: if the library or a CUDA
+device is missing, the calls raise.
+
+PyTorch is used for device memory (torch tensors may be passed as device
+pointers) and nothing else.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_PATH = os.path.join(_HERE, "lib", "libadimaxwell.so")
+SOURCES = [os.path.join(_HERE, "csrc", "adi_maxwell.cu"), os.path.join(_HERE, "csrc", "kernels.cuh"),
+           os.path.join(_ROOT, "include", "adi_maxwell.h")]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+ADI_OK, ADI_ERR_ARG, ADI_ERR_STATE, ADI_ERR_SINGULAR, ADI_ERR_CUDA, ADI_ERR_NCCL, ADI_ERR_OOM = range(7)
+ADI_BC_PEC, ADI_BC_NATURAL = 0, 1
+K_CLASSES = ["rhs_e", "rhs_h", "sweep_mass", "sweep_mod", "other"]
+
+EXPORTS = [
+    "adi_create", "adi_destroy", "adi_layout", "adi_set_tau", "adi_set_materials", "adi_set_materials_tf",
+    "adi_set_fields", "adi_get_fields", "adi_set_source", "adi_set_point_source", "adi_step", "adi_synchronize",
+    "adi_step_index", "adi_launches_per_step", "adi_stream", "adi_last_error", "adi_set_timing",
+    "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
+    "adi_debug_rhs_h", "adi_debug_solve_e",
+]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libadimaxwell.so in-tree for sm_100a (nvcc; no GPU needed)."""
+    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    newest = max(os.path.getmtime(s) for s in SOURCES)
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        tmp = LIB_PATH + ".tmp"
+        cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, SOURCES[0]]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class AdiConfig(C.Structure):
+    _fields_ = [("n", C.c_int32), ("p", C.c_int32), ("tau", C.c_double), ("bc", C.c_int32),
+                ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("stream", C.c_void_p)]
+
+
+_lib = None
+_lock = threading.Lock()
+_dp = C.POINTER(C.c_double)
+
+
+def lib():
+    """Load libadimaxwell.so (raises if it is missing -- no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} not built: run __graft_entry__.build() (nvcc, sm_100a)")
+            L = C.CDLL(LIB_PATH)
+            L.adi_create.argtypes = [C.POINTER(AdiConfig), C.POINTER(C.c_void_p)]
+            L.adi_destroy.argtypes = [C.c_void_p]
+            L.adi_destroy.restype = None
+            L.adi_layout.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.adi_set_tau.argtypes = [C.c_void_p, C.c_double]
+            L.adi_set_materials.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_set_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_set_fields.argtypes = [C.c_void_p, C.c_void_p]
+            L.adi_get_fields.argtypes = [C.c_void_p, C.c_void_p]
+            L.adi_set_source.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+            L.adi_set_point_source.argtypes = [C.c_void_p, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                               C.c_void_p, C.c_int64]
+            L.adi_step.argtypes = [C.c_void_p, C.c_int64]
+            L.adi_synchronize.argtypes = [C.c_void_p]
+            L.adi_step_index.argtypes = [C.c_void_p]
+            L.adi_step_index.restype = C.c_int64
+            L.adi_launches_per_step.argtypes = [C.c_void_p]
+            L.adi_launches_per_step.restype = C.c_int64
+            L.adi_stream.argtypes = [C.c_void_p]
+            L.adi_stream.restype = C.c_void_p
+            L.adi_last_error.restype = C.c_char_p
+            L.adi_set_timing.argtypes = [C.c_void_p, C.c_int32]
+            L.adi_timing_report.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_debug_matrices.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_debug_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_debug_sweep.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+            L.adi_debug_rhs_e.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+            L.adi_debug_rhs_h.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_debug_solve_e.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+            _lib = L
+        return _lib
+
+
+class AdiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"adi status {status}: {msg}")
+        self.status = status
+
+
+def _addr(x) -> int:
+    """Address of a host numpy array or a torch tensor (host or CUDA)."""
+    if isinstance(x, np.ndarray):
+        assert x.dtype == np.float64 and x.flags["C_CONTIGUOUS"], "need contiguous float64"
+        return x.ctypes.data
+    # torch.Tensor
+    assert x.dtype.itemsize == 8 and x.is_contiguous(), "need contiguous float64 tensor"
+    return x.data_ptr()
+
+
+def _as_f64(x):
+    if isinstance(x, np.ndarray):
+        return np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    return x
+
+
+def _ptr_array(objs):
+    arr = (C.c_void_p * len(objs))()
+    for i, o in enumerate(objs):
+        arr[i] = None if o is None else _addr(o)
+    return arr
+
+
+class Patch:
+    """One n x n x n patch on one B200 (device memory owned by the library)."""
+
+    def __init__(self, n: int, p: int, tau: float, bc: int = ADI_BC_PEC, device: int = 0):
+        L = lib()
+        self._L = L
+        cfg = AdiConfig(int(n), int(p), float(tau), int(bc), int(device), 0, 1, None)
+        h = C.c_void_p()
+        self._check(L.adi_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.n, self.p, self.tau, self.bc = int(n), int(p), float(tau), int(bc)
+        self.N = self.n + self.p
+        self.U = self.N ** 3
+
+    def _check(self, st: int):
+        if st != ADI_OK:
+            raise AdiError(st, self._L.adi_last_error().decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.adi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- setup -------------------------------------------------------------
+    def set_tau(self, tau: float):
+        self._check(self._L.adi_set_tau(self.h, float(tau)))
+        self.tau = float(tau)
+
+    def set_materials(self, eps_elem, mu_elem=None):
+        e, m = _as_f64(eps_elem), (None if mu_elem is None else _as_f64(mu_elem))
+        self._check(self._L.adi_set_materials(self.h, _addr(e), None if m is None else _addr(m)))
+
+    def set_materials_tf(self, eps_tf, mu_tf=None):
+        e, m = _as_f64(eps_tf), (None if mu_tf is None else _as_f64(mu_tf))
+        self._check(self._L.adi_set_materials_tf(self.h, _addr(e), None if m is None else _addr(m)))
+
+    def set_fields(self, fields):
+        fs = [_as_f64(f) for f in fields]
+        assert len(fs) == 6
+        self._check(self._L.adi_set_fields(self.h, _ptr_array(fs)))
+
+    def get_fields(self, out=None):
+        if out is None:
+            out = [np.empty(self.U) for _ in range(6)]
+        self._check(self._L.adi_get_fields(self.h, _ptr_array(out)))
+        return out
+
+    def set_source(self, loads, signal):
+        ls = [None if l is None else _as_f64(l) for l in loads]
+        sig = _as_f64(signal)
+        self._check(self._L.adi_set_source(self.h, _ptr_array(ls), _addr(sig), int(len(sig))))
+
+    def set_point_source(self, comp: int, pos, signal):
+        sig = _as_f64(signal)
+        self._check(self._L.adi_set_point_source(self.h, int(comp), float(pos[0]), float(pos[1]), float(pos[2]),
+                                                 _addr(sig), int(len(sig))))
+
+    # ---- stepping ------------------------------------------------------------
+    def step(self, k: int = 1):
+        self._check(self._L.adi_step(self.h, int(k)))
+
+    def synchronize(self):
+        self._check(self._L.adi_synchronize(self.h))
+
+    @property
+    def step_index(self) -> int:
+        return int(self._L.adi_step_index(self.h))
+
+    @property
+    def launches_per_step(self) -> int:
+        return int(self._L.adi_launches_per_step(self.h))
+
+    @property
+    def stream(self) -> int:
+        return int(self._L.adi_stream(self.h) or 0)
+
+    def set_timing(self, enable: bool):
+        self._check(self._L.adi_set_timing(self.h, int(bool(enable))))
+
+    def timing_report(self):
+        ms = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
+        self._check(self._L.adi_timing_report(self.h, ms, n))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(K_CLASSES)}
+
+    # ---- test-only -------------------------------------------------------------
+    def matrices(self):
+        N = self.N
+        M, S, A = (np.zeros((N, N)) for _ in range(3))
+        self._check(self._L.adi_debug_matrices(self.h, _addr(M), _addr(S), _addr(A)))
+        return M, S, A
+
+    def materials_tf(self):
+        e, m = np.zeros(self.U), np.zeros(self.U)
+        self._check(self._L.adi_debug_materials_tf(self.h, _addr(e), _addr(m)))
+        return e, m
+
+    def sweep(self, comp: int, axis: int, modified: bool, rhs):
+        r = _as_f64(rhs)
+        out = np.zeros(self.U)
+        self._check(self._L.adi_debug_sweep(self.h, int(comp), int(axis), int(bool(modified)), _addr(r), _addr(out)))
+        return out
+
+    def solve_e(self, s: int, d: int, rhs):
+        r = _as_f64(rhs)
+        out = np.zeros(self.U)
+        self._check(self._L.adi_debug_solve_e(self.h, int(s), int(d), _addr(r), _addr(out)))
+        return out
+
+    def rhs_e(self, s: int):
+        R = [np.zeros(self.U) for _ in range(3)]
+        self._check(self._L.adi_debug_rhs_e(self.h, int(s), _ptr_array(R)))
+        return R
+
+    def rhs_h(self, s: int, Eo, En):
+        G = [np.zeros(self.U) for _ in range(3)]
+        eo = [_as_f64(x) for x in Eo]
+        en = [_as_f64(x) for x in En]
+        self._check(self._L.adi_debug_rhs_h(self.h, int(s), _ptr_array(eo), _ptr_array(en), _ptr_array(G)))
+        return G

@@ -1,0 +1,1155 @@
+// adi_maxwell.cu -- libadimaxwell.so: C ABI (include/adi_maxwell.h) and host
+// orchestration of the sm_100a ADI-IGA Maxwell step (arXiv 2103.06998).
+//
+// Host side: 1D B-spline Galerkin matrices (D4, D11), constant mass
+// factorisations, material map weights (D6), the per-step launch sequence
+// (SURVEY §8(a) a1-a8), CUDA-graph capture of one step, per-kernel timing.
+// Device side: kernels.cuh.  Nothing here is shared with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/adi_maxwell.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+adi_status fail(adi_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+// 1D B-spline space on [0,1]: open uniform knots, degree p, C^{p-1}
+// ---------------------------------------------------------------------------
+struct Space1D {
+  int n, p, N;
+  std::vector<double> t;
+  explicit Space1D(int n_, int p_) : n(n_), p(p_), N(n_ + p_), t(n_ + 2 * p_ + 1) {
+    for (int i = 0; i <= p; i++) t[i] = 0.0, t[n + p + i] = 1.0;
+    for (int e = 1; e < n; e++) t[p + e] = double(e) / double(n);
+  }
+  // knot span index mu with t[mu] <= x < t[mu+1], mu in [p, n+p-1]
+  int span(double x) const {
+    if (x >= 1.0) return n + p - 1;
+    if (x <= 0.0) return p;
+    int e = (int)std::floor(x * n);
+    e = std::min(std::max(e, 0), n - 1);
+    int mu = p + e;
+    while (mu > p && x < t[mu]) mu--;
+    while (mu < n + p - 1 && x >= t[mu + 1]) mu++;
+    return mu;
+  }
+  // the p+1 non-zero basis functions B_{mu-p..mu}(x) and first derivatives
+  // (triangular de Boor scheme with left/right differences)
+  void eval(double x, int mu, double* val, double* der) const {
+    std::vector<double> left(p + 1), right(p + 1);
+    std::vector<std::vector<double>> ndu(p + 1, std::vector<double>(p + 1, 0.0));
+    ndu[0][0] = 1.0;
+    for (int j = 1; j <= p; j++) {
+      left[j] = x - t[mu + 1 - j];
+      right[j] = t[mu + j] - x;
+      double saved = 0.0;
+      for (int r = 0; r < j; r++) {
+        ndu[j][r] = right[r + 1] + left[j - r];  // lower triangle: knot differences
+        double tmp = ndu[r][j - 1] / ndu[j][r];
+        ndu[r][j] = saved + right[r + 1] * tmp;  // upper triangle: basis values
+        saved = left[j - r] * tmp;
+      }
+      ndu[j][j] = saved;
+    }
+    for (int r = 0; r <= p; r++) val[r] = ndu[r][p];
+    // first derivative: p * (N_{r,p-1}/(t_{r+p}-t_r) - N_{r+1,p-1}/(t_{r+p+1}-t_{r+1}))
+    for (int r = 0; r <= p; r++) {
+      double d = 0.0;
+      if (r >= 1) d += ndu[r - 1][p - 1] / ndu[p][r - 1];
+      if (r <= p - 1) d -= ndu[r][p - 1] / ndu[p][r];
+      der[r] = d * p;
+    }
+  }
+};
+
+// Gauss-Legendre rule on [0,1] with q points (Newton on the three-term recurrence)
+void gauss01(int q, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(q, 0.0);
+  w.assign(q, 0.0);
+  for (int i = 0; i < q; i++) {
+    double z = std::cos(M_PI * (4.0 * i + 3.0) / (4.0 * q + 2.0));
+    double dp = 1.0;
+    for (int it = 0; it < 64; it++) {
+      double P0 = 1.0, P1 = z;
+      for (int k = 2; k <= q; k++) {
+        double P2 = ((2.0 * k - 1.0) * z * P1 - (k - 1.0) * P0) / k;
+        P0 = P1;
+        P1 = P2;
+      }
+      if (q == 1) { P1 = z; P0 = 1.0; }
+      dp = q * (P0 - z * P1) / (1.0 - z * z);
+      double dz = P1 / dp;
+      z -= dz;
+      if (std::fabs(dz) <= 1e-17) break;
+    }
+    double P0 = 1.0, P1 = z;
+    for (int k = 2; k <= q; k++) {
+      double P2 = ((2.0 * k - 1.0) * z * P1 - (k - 1.0) * P0) / k;
+      P0 = P1;
+      P1 = P2;
+    }
+    if (q == 1) { P1 = z; P0 = 1.0; }
+    dp = q * (P0 - z * P1) / (1.0 - z * z);
+    x[i] = 0.5 * (1.0 - z);
+    w[i] = 1.0 / ((1.0 - z * z) * dp * dp);  // (2 / ((1-z^2) P'^2)) / 2
+  }
+}
+
+// Dense 1D matrices (row = test function l, column = trial function i):
+//   M_li = int B_l B_i, S_li = int B_l' B_i', A_li = int B_l B_i'   (D4)
+void assemble_1d(const Space1D& sp, std::vector<double>& M, std::vector<double>& S, std::vector<double>& A) {
+  const int N = sp.N, p = sp.p;
+  M.assign((size_t)N * N, 0.0);
+  S.assign((size_t)N * N, 0.0);
+  A.assign((size_t)N * N, 0.0);
+  std::vector<double> gx, gw;
+  gauss01(p + 1, gx, gw);  // exact: integrands have degree <= 2p (D11)
+  std::vector<double> v(p + 1), d(p + 1);
+  for (int e = 0; e < sp.n; e++) {
+    const double a = sp.t[p + e], h = sp.t[p + e + 1] - a;
+    for (size_t g = 0; g < gx.size(); g++) {
+      const double x = a + h * gx[g], wt = h * gw[g];
+      sp.eval(x, p + e, v.data(), d.data());
+      for (int r = 0; r <= p; r++)
+        for (int c = 0; c <= p; c++) {
+          const size_t I = (size_t)(e + r) * N + (e + c);
+          M[I] += wt * v[r] * v[c];
+          S[I] += wt * d[r] * d[c];
+          A[I] += wt * v[r] * d[c];
+        }
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Patch
+// ---------------------------------------------------------------------------
+struct adi_patch_s {
+  adi_config cfg{};
+  int n = 0, p = 0, N = 0, W = 0;
+  int64_t U = 0;
+  double tau = 0.0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  adi_status poison = ADI_OK;
+  std::vector<double> M, S, A;  // dense host copies
+  std::vector<double> wmat;     // material weights N x n (D6)
+  double* d_tab = nullptr;      // band tables (4 ops)
+  double* d_fac[2] = {nullptr, nullptr};  // mass LU, range variant 0 = [0,N), 1 = [1,N-1)
+  double* d_Mb[2] = {nullptr, nullptr};
+  double* d_Sb[2] = {nullptr, nullptr};
+  double* F[6] = {};
+  double* R[3] = {};
+  double* G[3] = {};
+  double *a = nullptr, *b = nullptr, *c = nullptr, *epsh = nullptr, *muh = nullptr;
+  double* scr = nullptr;
+  int64_t scr_pitch = 0;  // nfpad max over axes
+  double* load[3] = {};
+  double* signal = nullptr;
+  int64_t nsig = 0;
+  int64_t* d_step = nullptr;
+  int64_t step_index = 0;
+  bool have_fields = false;
+  cudaGraphExec_t graph = nullptr;
+  bool timing = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  std::vector<cudaEvent_t> ev_free;
+  double t_ms[ADI_K_NCLASS] = {};
+  int64_t t_n[ADI_K_NCLASS] = {};
+  int64_t launches_per_step = 0;
+  int64_t launch_counter = 0;
+  int nsm = 148;
+};
+
+namespace {
+
+#define CUDA_TRY(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess) {                                                                        \
+      return fail(ADI_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    }                                                                                               \
+  } while (0)
+
+adi_status poison(adi_patch P, adi_status st) {
+  if (st == ADI_ERR_CUDA || st == ADI_ERR_NCCL) P->poison = st;
+  return st;
+}
+
+// PEC active range of component comp along axis (D1)
+void active_range(const adi_patch P, int comp, int axis, int& lo, int& hi) {
+  lo = 0;
+  hi = P->N;
+  if (P->cfg.bc == ADI_BC_PEC && comp < 3 && axis != comp) {
+    lo = 1;
+    hi = P->N - 1;
+  }
+}
+
+// stiffened axis of E component d in substep s: K1 E1->y, E2->z, E3->x;
+// K2 E1->z, E2->x, E3->y  -- i.e. (d+1)%3 and (d+2)%3.
+int stiff_axis(int s, int d) { return s == 1 ? (d + 1) % 3 : (d + 2) % 3; }
+
+// ---- timing helpers ---------------------------------------------------------
+cudaEvent_t get_event(adi_patch P) {
+  if (!P->ev_free.empty()) {
+    cudaEvent_t e = P->ev_free.back();
+    P->ev_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct LaunchScope {
+  adi_patch P;
+  int cls;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  LaunchScope(adi_patch P_, int cls_) : P(P_), cls(cls_) {
+    P->launch_counter++;
+    if (P->timing) {
+      e0 = get_event(P);
+      e1 = get_event(P);
+      cudaEventRecord(e0, P->stream);
+    }
+  }
+  ~LaunchScope() {
+    if (P->timing) {
+      cudaEventRecord(e1, P->stream);
+      P->ev_used.push_back({cls, {e0, e1}});
+    }
+  }
+};
+
+// ---- launches ---------------------------------------------------------------
+template <int PP>
+adi_status launch_rhs_p(adi_patch P, const adi::RhsArgs& args, int nt) {
+  const int N = P->N;
+  dim3 block(adi::RHS_TX, adi::RHS_TY);
+  dim3 grid((N + adi::RHS_TX - 1) / adi::RHS_TX, (N + adi::RHS_TY - 1) / adi::RHS_TY,
+            (N + args.kchunk - 1) / args.kchunk);
+  switch (nt) {
+    case 3: adi::rhs_kernel<PP, 3><<<grid, block, 0, P->stream>>>(args); break;
+    case 4: adi::rhs_kernel<PP, 4><<<grid, block, 0, P->stream>>>(args); break;
+    default: return fail(ADI_ERR_ARG, "rhs: unsupported term count %d", nt);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
+adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int nt, int comp, int cls) {
+  args.N = P->N;
+  args.kchunk = P->N <= 96 ? 16 : 64;
+  args.tab = P->d_tab;
+  args.a = P->a;
+  args.b = P->b;
+  args.c = P->c;
+  args.step = P->d_step;
+  for (int ax = 0; ax < 3; ax++) active_range(P, comp, ax, args.lo[ax], args.hi[ax]);
+  LaunchScope ls(P, cls);
+  switch (P->p) {
+    case 1: return launch_rhs_p<1>(P, args, nt);
+    case 2: return launch_rhs_p<2>(P, args, nt);
+    case 3: return launch_rhs_p<3>(P, args, nt);
+    case 4: return launch_rhs_p<4>(P, args, nt);
+    case 5: return launch_rhs_p<5>(P, args, nt);
+  }
+  return fail(ADI_ERR_ARG, "rhs: bad p");
+}
+
+adi::RhsTerm term(const double* u, int ox, int oy, int oz, int scale, double sign) {
+  adi::RhsTerm t;
+  t.u = u;
+  t.op[0] = ox;
+  t.op[1] = oy;
+  t.op[2] = oz;
+  t.scale = scale;
+  t.sign = sign;
+  return t;
+}
+
+// Operator triple with A on axis `ax` and M elsewhere.
+void deriv_ops(int ax, int op[3]) {
+  for (int k = 0; k < 3; k++) op[k] = (k == ax) ? adi::OP_A : adi::OP_M;
+}
+
+// RHS of the E system of component d, substep s (a1/a5):
+//   R_d = M^3 E_d + a [ d_{d+1} H_{d+2} - d_{d+2} H_{d+1} ] + c (A on d, B on sigma) E_sigma
+// with sigma the stiffened axis (discrete1/discrete3; dupa1ab P:373-386).
+adi_status rhs_e(adi_patch P, int s, int d, const double* const E[3], const double* const H[3], double* out) {
+  adi::RhsArgs args{};
+  int op[3];
+  args.term[0] = term(E[d], adi::OP_M, adi::OP_M, adi::OP_M, adi::SC_ONE, 1.0);
+  deriv_ops((d + 1) % 3, op);
+  args.term[1] = term(H[(d + 2) % 3], op[0], op[1], op[2], adi::SC_A, 1.0);
+  deriv_ops((d + 2) % 3, op);
+  args.term[2] = term(H[(d + 1) % 3], op[0], op[1], op[2], adi::SC_A, -1.0);
+  const int sg = stiff_axis(s, d);
+  int rop[3];
+  for (int k = 0; k < 3; k++) rop[k] = adi::OP_M;
+  rop[d] = adi::OP_A;
+  rop[sg] = adi::OP_B;
+  args.term[3] = term(E[sg], rop[0], rop[1], rop[2], adi::SC_C, 1.0);
+  args.load = P->load[d];
+  args.signal = P->signal;
+  args.nsig = P->nsig;
+  args.out = out;
+  return launch_rhs(P, args, 4, d, ADI_K_RHS_E);
+}
+
+// RHS of the H system of component d, substep s (a3/a7):
+//   s=1: G_d = M^3 H_d - b d_{d+1} Eo_{d+2} + b d_{d+2} En_{d+1}   (discrete2)
+//   s=2: G_d = M^3 H_d + b d_{d+2} Eo_{d+1} - b d_{d+1} En_{d+2}   (discrete4 with D2)
+adi_status rhs_h(adi_patch P, int s, int d, const double* Hd, const double* const Eo[3], const double* const En[3],
+                 double* out) {
+  adi::RhsArgs args{};
+  int op[3];
+  args.term[0] = term(Hd, adi::OP_M, adi::OP_M, adi::OP_M, adi::SC_ONE, 1.0);
+  if (s == 1) {
+    deriv_ops((d + 1) % 3, op);
+    args.term[1] = term(Eo[(d + 2) % 3], op[0], op[1], op[2], adi::SC_B, -1.0);
+    deriv_ops((d + 2) % 3, op);
+    args.term[2] = term(En[(d + 1) % 3], op[0], op[1], op[2], adi::SC_B, 1.0);
+  } else {
+    deriv_ops((d + 2) % 3, op);
+    args.term[1] = term(Eo[(d + 1) % 3], op[0], op[1], op[2], adi::SC_B, 1.0);
+    deriv_ops((d + 1) % 3, op);
+    args.term[2] = term(En[(d + 2) % 3], op[0], op[1], op[2], adi::SC_B, -1.0);
+  }
+  args.out = out;
+  return launch_rhs(P, args, 3, 3 + d, ADI_K_RHS_H);
+}
+
+int64_t ntiles_axis(int N, int axis) {
+  const int64_t NN = (int64_t)N * N;
+  if (axis == 1) return (int64_t)N * ((N + 31) / 32);
+  return (NN + 31) / 32;
+}
+
+template <int PP>
+adi_status launch_sweep_p(adi_patch P, const adi::SweepArgs& A, bool modified) {
+  const int W = 2 * PP + 1;
+  const int nsm = P->nsm;
+  size_t smem = (size_t)(modified ? 2 : 1) * P->N * W * sizeof(double);
+  if (A.axis == 0) smem += (size_t)adi::SWEEP_WARPS * 32 * 33 * sizeof(double);
+  const int64_t blocks_needed = (A.ntiles + adi::SWEEP_WARPS - 1) / adi::SWEEP_WARPS;
+  const int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)nsm * 16);
+  if (modified) {
+    constexpr int CH = 16;
+    auto k = adi::sweep_mod_kernel<PP, CH>;
+    k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
+  } else {
+    constexpr int CH = 32;
+    auto k = adi::sweep_mass_kernel<PP, CH>;
+    k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
+template <int PP>
+adi_status sweep_attrs_p(adi_patch P) {
+  const int W = 2 * PP + 1;
+  const int mass = (int)(((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * 32 * 33) * sizeof(double));
+  const int mod = (int)(((size_t)2 * P->N * W + (size_t)adi::SWEEP_WARPS * 32 * 33) * sizeof(double));
+  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mass_kernel<PP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass));
+  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mod_kernel<PP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mod));
+  return ADI_OK;
+}
+
+adi_status sweep_attrs(adi_patch P) {
+  switch (P->p) {
+    case 1: return sweep_attrs_p<1>(P);
+    case 2: return sweep_attrs_p<2>(P);
+    case 3: return sweep_attrs_p<3>(P);
+    case 4: return sweep_attrs_p<4>(P);
+    case 5: return sweep_attrs_p<5>(P);
+  }
+  return fail(ADI_ERR_ARG, "bad p");
+}
+
+// One sweep along `axis` for component comp (active set per D1), in place on u
+// (or in -> out).  modified: M + diag(c) S per row (P:545/555/581), else M.
+adi_status sweep(adi_patch P, int comp, int axis, bool modified, const double* in, double* out) {
+  adi::SweepArgs A{};
+  A.N = P->N;
+  A.axis = axis;
+  active_range(P, comp, axis, A.lo, A.hi);
+  const int var = (A.lo == 0) ? 0 : 1;
+  A.ntiles = (int)ntiles_axis(P->N, axis);
+  A.nfpad = (int64_t)A.ntiles * 32;
+  A.in = in;
+  A.out = out;
+  A.scr = P->scr;
+  A.fac = P->d_fac[var];
+  A.Mb = P->d_Mb[var];
+  A.Sb = P->d_Sb[var];
+  A.c = P->c;
+  LaunchScope ls(P, modified ? ADI_K_SWEEP_MOD : ADI_K_SWEEP_MASS);
+  switch (P->p) {
+    case 1: return launch_sweep_p<1>(P, A, modified);
+    case 2: return launch_sweep_p<2>(P, A, modified);
+    case 3: return launch_sweep_p<3>(P, A, modified);
+    case 4: return launch_sweep_p<4>(P, A, modified);
+    case 5: return launch_sweep_p<5>(P, A, modified);
+  }
+  return fail(ADI_ERR_ARG, "sweep: bad p");
+}
+
+// E solve of component d, substep s: stiffened axis first (row-modified),
+// then the two mass sweeps in ascending axis order (D7).
+adi_status solve_e(adi_patch P, int s, int d, const double* in, double* out) {
+  const int sg = stiff_axis(s, d);
+  adi_status st = sweep(P, d, sg, true, in, out);
+  if (st) return st;
+  for (int ax = 0; ax < 3; ax++) {
+    if (ax == sg) continue;
+    if ((st = sweep(P, d, ax, false, out, out))) return st;
+  }
+  return ADI_OK;
+}
+
+// H solve: (M (x) M (x) M)^{-1}, three mass sweeps
+adi_status solve_h(adi_patch P, int d, double* u) {
+  adi_status st;
+  for (int ax = 0; ax < 3; ax++)
+    if ((st = sweep(P, 3 + d, ax, false, u, u))) return st;
+  return ADI_OK;
+}
+
+// One substep (ALG-2 / ALG-7): RHS_E -> E solves -> RHS_H -> H solves, then
+// rotate buffers (new E lives in R, new H in G).
+adi_status substep(adi_patch P, int s) {
+  adi_status st;
+  const double* E[3] = {P->F[0], P->F[1], P->F[2]};
+  const double* H[3] = {P->F[3], P->F[4], P->F[5]};
+  for (int d = 0; d < 3; d++)
+    if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
+  for (int d = 0; d < 3; d++)
+    if ((st = solve_e(P, s, d, P->R[d], P->R[d]))) return st;
+  const double* En[3] = {P->R[0], P->R[1], P->R[2]};
+  for (int d = 0; d < 3; d++)
+    if ((st = rhs_h(P, s, d, H[d], E, En, P->G[d]))) return st;
+  for (int d = 0; d < 3; d++)
+    if ((st = solve_h(P, d, P->G[d]))) return st;
+  for (int d = 0; d < 3; d++) {
+    std::swap(P->F[d], P->R[d]);
+    std::swap(P->F[3 + d], P->G[d]);
+  }
+  return ADI_OK;
+}
+
+adi_status full_step(adi_patch P) {
+  adi_status st;
+  if ((st = substep(P, 1))) return st;
+  if ((st = substep(P, 2))) return st;
+  {
+    LaunchScope ls(P, ADI_K_OTHER);
+    adi::increment_kernel<<<1, 1, 0, P->stream>>>(P->d_step);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return ADI_OK;
+}
+
+// host band tables and mass factorisations ----------------------------------
+void band_from_dense(const std::vector<double>& X, bool transpose, int N, int p, int lo, int hi, double* out) {
+  const int W = 2 * p + 1;
+  for (int r = 0; r < N; r++)
+    for (int q = 0; q < W; q++) {
+      const int c = r - p + q;
+      double v = 0.0;
+      if (c >= lo && c < hi && r >= lo && r < hi) v = transpose ? X[(size_t)c * N + r] : X[(size_t)r * N + c];
+      out[(size_t)r * W + q] = v;
+    }
+}
+
+// banded LU (no pivoting; M is SPD) of M restricted to [lo,hi):
+// fac[kk*W + {0..p-1}] = l_{kk,kk-1-q}, fac[kk*W+p] = 1/u_kk, fac[kk*W+p+1+q] = u_{kk,kk+1+q}
+bool mass_factor(const std::vector<double>& M, int N, int p, int lo, int hi, std::vector<double>& fac) {
+  const int W = 2 * p + 1, m = hi - lo;
+  fac.assign((size_t)N * W, 0.0);
+  std::vector<double> Ub((size_t)m * (p + 1), 0.0);  // U rows: Ub[k*(p+1)+q] = u_{k,k+q}
+  for (int k = 0; k < m; k++) {
+    double a[32];
+    for (int q = -p; q <= p; q++) {
+      const int j = k + q;
+      a[q + p] = (j >= 0 && j < m) ? M[(size_t)(lo + k) * N + (lo + j)] : 0.0;
+    }
+    double l[16] = {0};
+    for (int mm = p; mm >= 1; mm--) {
+      if (k - mm < 0) { l[mm] = 0.0; continue; }
+      double s = a[p - mm];
+      for (int mp = p; mp > mm; mp--)
+        if (k - mp >= 0) s -= l[mp] * Ub[(size_t)(k - mp) * (p + 1) + (mp - mm)];
+      l[mm] = s / Ub[(size_t)(k - mm) * (p + 1)];
+    }
+    for (int q = 0; q <= p; q++) {
+      double s = a[p + q];
+      for (int mm = 1; mm <= p; mm++)
+        if (k - mm >= 0 && mm + q <= p) s -= l[mm] * Ub[(size_t)(k - mm) * (p + 1) + mm + q];
+      Ub[(size_t)k * (p + 1) + q] = s;
+    }
+    double rowmax = 0.0;
+    for (int q = 0; q < 2 * p + 1; q++) rowmax = std::max(rowmax, std::fabs(a[q]));
+    if (!(std::fabs(Ub[(size_t)k * (p + 1)]) >= 1e-14 * rowmax)) return false;
+    double* fr = &fac[(size_t)k * W];
+    for (int q = 0; q < p; q++) fr[q] = l[q + 1];
+    fr[p] = 1.0 / Ub[(size_t)k * (p + 1)];
+    for (int q = 0; q < p; q++) fr[p + 1 + q] = Ub[(size_t)k * (p + 1) + 1 + q];
+  }
+  return true;
+}
+
+bool is_device_ptr(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+adi_status copy_in(adi_patch P, double* dst, const double* src, int64_t n) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDefault, P->stream));
+  if (!is_device_ptr(src)) CUDA_TRY(cudaStreamSynchronize(P->stream));
+  return ADI_OK;
+}
+
+void drop_graph(adi_patch P) {
+  if (P->graph) {
+    cudaGraphExecDestroy(P->graph);
+    P->graph = nullptr;
+  }
+}
+
+adi_status check_positive(adi_patch P, const double* d, int64_t n, const char* what) {
+  unsigned long long* bad;
+  CUDA_TRY(cudaMallocAsync(&bad, sizeof(unsigned long long), P->stream));
+  unsigned long long init = ~0ull;
+  CUDA_TRY(cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream));
+  adi::check_positive_kernel<<<592, 256, 0, P->stream>>>(d, n, bad);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaFreeAsync(bad, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  if (h != ~0ull) return fail(ADI_ERR_ARG, "%s[%llu] is not a finite value > 0", what, h);
+  return ADI_OK;
+}
+
+// D12 gate: scan every row-modified family for tiny pivots (no pivoting on the GPU)
+adi_status pivot_scan(adi_patch P) {
+  unsigned long long* bad;
+  CUDA_TRY(cudaMallocAsync(&bad, sizeof(unsigned long long), P->stream));
+  for (int s = 1; s <= 2; s++)
+    for (int d = 0; d < 3; d++) {
+      const int ax = stiff_axis(s, d);
+      adi::SweepArgs A{};
+      A.N = P->N;
+      A.axis = ax;
+      active_range(P, d, ax, A.lo, A.hi);
+      const int var = A.lo == 0 ? 0 : 1;
+      A.ntiles = (int)ntiles_axis(P->N, ax);
+      A.nfpad = (int64_t)A.ntiles * 32;
+      A.Mb = P->d_Mb[var];
+      A.Sb = P->d_Sb[var];
+      A.c = P->c;
+      unsigned long long init = ~0ull;
+      CUDA_TRY(cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream));
+      const unsigned grid = (unsigned)std::min<int64_t>((A.ntiles + 7) / 8, 148 * 8);
+      switch (P->p) {
+        case 1: adi::pivot_scan_kernel<1><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
+        case 2: adi::pivot_scan_kernel<2><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
+        case 3: adi::pivot_scan_kernel<3><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
+        case 4: adi::pivot_scan_kernel<4><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
+        case 5: adi::pivot_scan_kernel<5><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
+      }
+      CUDA_TRY(cudaGetLastError());
+      unsigned long long h = 0;
+      CUDA_TRY(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, P->stream));
+      CUDA_TRY(cudaStreamSynchronize(P->stream));
+      if (h != ~0ull) {
+        cudaFreeAsync(bad, P->stream);
+        return fail(ADI_ERR_SINGULAR, "tiny pivot in row-modified sweep (component %d, substep %d, axis %d, fiber %llu)",
+                    d, s, ax, h);
+      }
+    }
+  CUDA_TRY(cudaFreeAsync(bad, P->stream));
+  return ADI_OK;
+}
+
+adi_status derive_abc(adi_patch P, double* epsh, double* muh) {
+  adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh, muh, P->tau, P->U, P->a, P->b, P->c);
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* adi_last_error(void) { return g_err.c_str(); }
+
+void adi_destroy(adi_patch P) {
+  if (!P) return;
+  cudaSetDevice(P->cfg.device);
+  if (P->stream) cudaStreamSynchronize(P->stream);
+  drop_graph(P);
+  auto f = [](void* x) { if (x) cudaFree(x); };
+  f(P->d_tab);
+  for (int v = 0; v < 2; v++) f(P->d_fac[v]), f(P->d_Mb[v]), f(P->d_Sb[v]);
+  for (int i = 0; i < 6; i++) f(P->F[i]);
+  for (int i = 0; i < 3; i++) f(P->R[i]), f(P->G[i]), f(P->load[i]);
+  f(P->a), f(P->b), f(P->c), f(P->epsh), f(P->muh), f(P->scr), f(P->signal), f(P->d_step);
+  for (auto& e : P->ev_used) cudaEventDestroy(e.second.first), cudaEventDestroy(e.second.second);
+  for (auto& e : P->ev_free) cudaEventDestroy(e);
+  if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+adi_status adi_create(const adi_config* cfg, adi_patch* out) {
+  if (!out) return fail(ADI_ERR_ARG, "adi_create: out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(ADI_ERR_ARG, "adi_create: cfg is NULL");
+  if (cfg->n < 1) return fail(ADI_ERR_ARG, "adi_create: n = %d < 1", cfg->n);
+  if (cfg->p < 1 || cfg->p > 5) return fail(ADI_ERR_ARG, "adi_create: p = %d outside 1..5", cfg->p);
+  if (!(cfg->tau > 0.0) || !std::isfinite(cfg->tau)) return fail(ADI_ERR_ARG, "adi_create: tau must be finite and > 0");
+  if (cfg->bc != ADI_BC_PEC && cfg->bc != ADI_BC_NATURAL) return fail(ADI_ERR_ARG, "adi_create: bad bc %d", cfg->bc);
+  if (cfg->nranks != 1 || cfg->rank != 0)
+    return fail(ADI_ERR_ARG, "adi_create: this build is single-rank (rank 0 of 1)");
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) return fail(ADI_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(e));
+  adi_patch P = new adi_patch_s();
+  P->cfg = *cfg;
+  P->n = cfg->n;
+  P->p = cfg->p;
+  P->N = cfg->n + cfg->p;
+  P->W = 2 * cfg->p + 1;
+  P->U = (int64_t)P->N * P->N * P->N;
+  P->tau = cfg->tau;
+  auto bail = [&](adi_status st) {
+    adi_destroy(P);
+    return st;
+  };
+  if (cfg->stream) {
+    P->stream = (cudaStream_t)cfg->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(ADI_ERR_CUDA, "cudaStreamCreate failed"));
+    P->own_stream = true;
+  }
+  const int N = P->N, p = P->p, W = P->W;
+  cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (sweep_attrs(P)) return bail(fail(ADI_ERR_ARG, "N = %d too large for the sweep kernels' shared memory", N));
+  Space1D sp(P->n, p);
+  assemble_1d(sp, P->M, P->S, P->A);
+  // material weights (D6): w[r*n+e] = int_{elem e} B_r / int B_r (Gauss q = p+1, exact)
+  {
+    P->wmat.assign((size_t)N * P->n, 0.0);
+    std::vector<double> gx, gw, v(p + 1), d(p + 1);
+    gauss01(p + 1, gx, gw);
+    for (int el = 0; el < P->n; el++) {
+      const double a = sp.t[p + el], h = sp.t[p + el + 1] - a;
+      for (size_t g = 0; g < gx.size(); g++) {
+        sp.eval(a + h * gx[g], p + el, v.data(), d.data());
+        for (int r = 0; r <= p; r++) P->wmat[(size_t)(el + r) * P->n + el] += h * gw[g] * v[r];
+      }
+    }
+    for (int r = 0; r < N; r++) {
+      double s = 0.0;
+      for (int el = 0; el < P->n; el++) s += P->wmat[(size_t)r * P->n + el];
+      for (int el = 0; el < P->n; el++) P->wmat[(size_t)r * P->n + el] /= s;
+    }
+  }
+  // band tables: M, A, B = A^T, S over the full range
+  std::vector<double> tab((size_t)4 * N * W);
+  band_from_dense(P->M, false, N, p, 0, N, &tab[(size_t)adi::OP_M * N * W]);
+  band_from_dense(P->A, false, N, p, 0, N, &tab[(size_t)adi::OP_A * N * W]);
+  band_from_dense(P->A, true, N, p, 0, N, &tab[(size_t)adi::OP_B * N * W]);
+  band_from_dense(P->S, false, N, p, 0, N, &tab[(size_t)adi::OP_S * N * W]);
+  auto dmalloc = [&](double** ptr, size_t n) -> bool {
+    if (cudaMalloc(ptr, n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      *ptr = nullptr;
+      return false;
+    }
+    return true;
+  };
+  if (!dmalloc(&P->d_tab, tab.size())) return bail(fail(ADI_ERR_OOM, "cudaMalloc band tables"));
+  cudaMemcpy(P->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
+  for (int var = 0; var < 2; var++) {
+    const int lo = var ? 1 : 0, hi = var ? N - 1 : N;
+    std::vector<double> fac, Mb((size_t)N * W), Sb((size_t)N * W);
+    if (var == 1 && N < 3) {
+      fac.assign((size_t)N * W, 0.0);
+    } else if (!mass_factor(P->M, N, p, lo, hi, fac)) {
+      return bail(fail(ADI_ERR_SINGULAR, "mass matrix factorisation: tiny pivot"));
+    }
+    // rows are indexed relative to lo in fac; Mb/Sb are indexed by absolute row
+    band_from_dense(P->M, false, N, p, lo, hi, Mb.data());
+    band_from_dense(P->S, false, N, p, lo, hi, Sb.data());
+    if (!dmalloc(&P->d_fac[var], fac.size()) || !dmalloc(&P->d_Mb[var], Mb.size()) || !dmalloc(&P->d_Sb[var], Sb.size()))
+      return bail(fail(ADI_ERR_OOM, "cudaMalloc factor tables"));
+    cudaMemcpy(P->d_fac[var], fac.data(), fac.size() * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(P->d_Mb[var], Mb.data(), Mb.size() * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(P->d_Sb[var], Sb.data(), Sb.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  const size_t U = (size_t)P->U;
+  for (int i = 0; i < 6; i++)
+    if (!dmalloc(&P->F[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc fields (%zu doubles)", U));
+  for (int i = 0; i < 3; i++)
+    if (!dmalloc(&P->R[i], U) || !dmalloc(&P->G[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc scratch fields"));
+  if (!dmalloc(&P->a, U) || !dmalloc(&P->b, U) || !dmalloc(&P->c, U) || !dmalloc(&P->epsh, U) || !dmalloc(&P->muh, U))
+    return bail(fail(ADI_ERR_OOM, "cudaMalloc material arrays"));
+  int64_t pitch = 0;
+  for (int ax = 0; ax < 3; ax++) pitch = std::max<int64_t>(pitch, ntiles_axis(N, ax) * 32);
+  P->scr_pitch = pitch;
+  if (!dmalloc(&P->scr, (size_t)(p + 2) * N * pitch)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep scratch"));
+  if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));
+  cudaMemset(P->d_step, 0, sizeof(int64_t));
+  for (int i = 0; i < 6; i++) cudaMemset(P->F[i], 0, U * sizeof(double));
+  // eps = mu = 1
+  adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->epsh, P->U, 1.0);
+  adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->muh, P->U, 1.0);
+  adi_status st = derive_abc(P, P->epsh, P->muh);
+  if (st) return bail(st);
+  e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "setup: %s", cudaGetErrorString(e)));
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "setup: %s", cudaGetErrorString(e)));
+  // launches per step: 2 x (3 rhs_e + 9 sweeps + 3 rhs_h + 9 sweeps) + 1 counter kernel
+  P->launches_per_step = 2 * (3 + 9 + 3 + 9) + 1;
+  *out = P;
+  return ADI_OK;
+}
+
+#define CHECK_PATCH(P)                                                 \
+  do {                                                                 \
+    if (!(P)) return fail(ADI_ERR_ARG, "patch is NULL");               \
+    if ((P)->poison) return fail((P)->poison, "patch is poisoned by an earlier CUDA error"); \
+    cudaSetDevice((P)->cfg.device);                                    \
+  } while (0)
+
+adi_status adi_layout(adi_patch P, int64_t* N, int64_t* k0, int64_t* k1) {
+  CHECK_PATCH(P);
+  if (N) *N = P->N;
+  if (k0) *k0 = 0;
+  if (k1) *k1 = P->N;
+  return ADI_OK;
+}
+
+adi_status adi_set_tau(adi_patch P, double tau) {
+  CHECK_PATCH(P);
+  if (!(tau > 0.0) || !std::isfinite(tau)) return fail(ADI_ERR_ARG, "adi_set_tau: tau must be finite and > 0");
+  const double old = P->tau;
+  P->tau = tau;
+  adi_status st = derive_abc(P, P->epsh, P->muh);
+  if (!st) st = pivot_scan(P);
+  if (st) {
+    P->tau = old;
+    derive_abc(P, P->epsh, P->muh);
+    cudaStreamSynchronize(P->stream);
+    return poison(P, st);
+  }
+  return ADI_OK;
+}
+
+static adi_status set_tf(adi_patch P, double* eps_new, double* mu_new) {
+  // eps_new / mu_new: device buffers (owned) holding validated values; swap in
+  std::swap(P->epsh, eps_new);
+  std::swap(P->muh, mu_new);
+  adi_status st = derive_abc(P, P->epsh, P->muh);
+  if (!st) st = pivot_scan(P);
+  if (st) {  // restore
+    std::swap(P->epsh, eps_new);
+    std::swap(P->muh, mu_new);
+    derive_abc(P, P->epsh, P->muh);
+  }
+  cudaStreamSynchronize(P->stream);
+  cudaFree(eps_new);
+  cudaFree(mu_new);
+  return st;
+}
+
+adi_status adi_set_materials_tf(adi_patch P, const double* eps_tf, const double* mu_tf) {
+  CHECK_PATCH(P);
+  if (!eps_tf) return fail(ADI_ERR_ARG, "adi_set_materials_tf: eps is NULL");
+  double *e = nullptr, *m = nullptr;
+  if (cudaMalloc(&e, P->U * sizeof(double)) != cudaSuccess || cudaMalloc(&m, P->U * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(e);
+    return fail(ADI_ERR_OOM, "adi_set_materials_tf: cudaMalloc");
+  }
+  adi_status st = copy_in(P, e, eps_tf, P->U);
+  if (!st) st = check_positive(P, e, P->U, "eps");
+  if (!st) {
+    if (mu_tf) {
+      st = copy_in(P, m, mu_tf, P->U);
+      if (!st) st = check_positive(P, m, P->U, "mu");
+    } else {
+      adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(m, P->U, 1.0);
+    }
+  }
+  if (st) {
+    cudaFree(e);
+    cudaFree(m);
+    return poison(P, st);
+  }
+  return poison(P, set_tf(P, e, m));
+}
+
+// element-wise -> per-test-function (D6): three separable passes on the GPU
+static adi_status map_elements(adi_patch P, const double* d_elem, double* d_out, const double* d_w) {
+  const int n = P->n, N = P->N;
+  double *t1 = nullptr, *t2 = nullptr;
+  CUDA_TRY(cudaMallocAsync(&t1, (size_t)n * n * N * sizeof(double), P->stream));
+  CUDA_TRY(cudaMallocAsync(&t2, (size_t)n * N * N * sizeof(double), P->stream));
+  adi::material_pass_kernel<<<148 * 8, 256, 0, P->stream>>>(d_elem, t1, d_w, n, N, P->p, 2, n, n, n);
+  adi::material_pass_kernel<<<148 * 8, 256, 0, P->stream>>>(t1, t2, d_w, n, N, P->p, 1, n, n, N);
+  adi::material_pass_kernel<<<148 * 8, 256, 0, P->stream>>>(t2, d_out, d_w, n, N, P->p, 0, n, N, N);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(t1, P->stream));
+  CUDA_TRY(cudaFreeAsync(t2, P->stream));
+  return ADI_OK;
+}
+
+adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* mu_elem) {
+  CHECK_PATCH(P);
+  if (!eps_elem) return fail(ADI_ERR_ARG, "adi_set_materials: eps is NULL");
+  const int64_t ne = (int64_t)P->n * P->n * P->n;
+  double *de = nullptr, *dw = nullptr, *e = nullptr, *m = nullptr;
+  adi_status st = ADI_OK;
+  if (cudaMalloc(&de, ne * sizeof(double)) != cudaSuccess || cudaMalloc(&dw, P->wmat.size() * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&e, P->U * sizeof(double)) != cudaSuccess || cudaMalloc(&m, P->U * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(de), cudaFree(dw), cudaFree(e), cudaFree(m);
+    return fail(ADI_ERR_OOM, "adi_set_materials: cudaMalloc");
+  }
+  cudaMemcpy(dw, P->wmat.data(), P->wmat.size() * sizeof(double), cudaMemcpyHostToDevice);
+  st = copy_in(P, de, eps_elem, ne);
+  if (!st) st = check_positive(P, de, ne, "eps");
+  if (!st) st = map_elements(P, de, e, dw);
+  if (!st) {
+    if (mu_elem) {
+      st = copy_in(P, de, mu_elem, ne);
+      if (!st) st = check_positive(P, de, ne, "mu");
+      if (!st) st = map_elements(P, de, m, dw);
+    } else {
+      adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(m, P->U, 1.0);
+    }
+  }
+  cudaStreamSynchronize(P->stream);
+  cudaFree(de);
+  cudaFree(dw);
+  if (st) {
+    cudaFree(e);
+    cudaFree(m);
+    return poison(P, st);
+  }
+  return poison(P, set_tf(P, e, m));
+}
+
+adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
+  CHECK_PATCH(P);
+  if (!f) return fail(ADI_ERR_ARG, "adi_set_fields: NULL array");
+  for (int c = 0; c < 6; c++)
+    if (!f[c]) return fail(ADI_ERR_ARG, "adi_set_fields: field %d is NULL", c);
+  for (int c = 0; c < 6; c++) {
+    adi_status st = copy_in(P, P->F[c], f[c], P->U);
+    if (st) return poison(P, st);
+    if (c < 3 && P->cfg.bc == ADI_BC_PEC) {
+      int lo[3], hi[3];
+      for (int ax = 0; ax < 3; ax++) active_range(P, c, ax, lo[ax], hi[ax]);
+      adi::pec_zero_kernel<<<148 * 8, 256, 0, P->stream>>>(P->F[c], P->N, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]);
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_set_fields: %s", cudaGetErrorString(e)));
+  P->have_fields = true;
+  return ADI_OK;
+}
+
+adi_status adi_get_fields(adi_patch P, double* const f[6]) {
+  CHECK_PATCH(P);
+  if (!f) return fail(ADI_ERR_ARG, "adi_get_fields: NULL array");
+  for (int c = 0; c < 6; c++) {
+    if (!f[c]) continue;
+    cudaError_t e = cudaMemcpyAsync(f[c], P->F[c], P->U * sizeof(double), cudaMemcpyDefault, P->stream);
+    if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_get_fields: %s", cudaGetErrorString(e)));
+  }
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_get_fields: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+adi_status adi_set_source(adi_patch P, const double* const load[3], const double* signal, int64_t nsig) {
+  CHECK_PATCH(P);
+  if (nsig < 0) return fail(ADI_ERR_ARG, "adi_set_source: nsig < 0");
+  drop_graph(P);
+  cudaStreamSynchronize(P->stream);
+  for (int d = 0; d < 3; d++) {
+    if (P->load[d]) cudaFree(P->load[d]);
+    P->load[d] = nullptr;
+  }
+  if (P->signal) cudaFree(P->signal);
+  P->signal = nullptr;
+  P->nsig = 0;
+  if (!load || !signal || nsig == 0) return ADI_OK;
+  for (int d = 0; d < 3; d++) {
+    if (!load[d]) continue;
+    if (cudaMalloc(&P->load[d], P->U * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ADI_ERR_OOM, "adi_set_source: cudaMalloc");
+    }
+    adi_status st = copy_in(P, P->load[d], load[d], P->U);
+    if (st) return poison(P, st);
+  }
+  if (cudaMalloc(&P->signal, nsig * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ADI_ERR_OOM, "adi_set_source: cudaMalloc signal");
+  }
+  adi_status st = copy_in(P, P->signal, signal, nsig);
+  if (st) return poison(P, st);
+  P->nsig = nsig;
+  cudaStreamSynchronize(P->stream);
+  return ADI_OK;
+}
+
+adi_status adi_set_point_source(adi_patch P, int32_t comp, double xs, double ys, double zs, const double* signal,
+                                int64_t nsig) {
+  CHECK_PATCH(P);
+  if (comp < 0 || comp > 2) return fail(ADI_ERR_ARG, "adi_set_point_source: comp %d outside 0..2", comp);
+  for (double x : {xs, ys, zs})
+    if (!(x >= 0.0 && x <= 1.0)) return fail(ADI_ERR_ARG, "adi_set_point_source: position outside [0,1]^3");
+  Space1D sp(P->n, P->p);
+  const int N = P->N, p = P->p;
+  std::vector<double> bx(N, 0.0), by(N, 0.0), bz(N, 0.0), v(p + 1), d(p + 1);
+  const double pos[3] = {xs, ys, zs};
+  std::vector<double>* outs[3] = {&bx, &by, &bz};
+  for (int ax = 0; ax < 3; ax++) {
+    const int mu = sp.span(pos[ax]);
+    sp.eval(pos[ax], mu, v.data(), d.data());
+    for (int r = 0; r <= p; r++) (*outs[ax])[mu - p + r] = v[r];
+  }
+  std::vector<double> L((size_t)P->U, 0.0);
+  for (int k = 0; k < N; k++)
+    for (int j = 0; j < N; j++)
+      for (int i = 0; i < N; i++) L[i + (size_t)N * (j + (size_t)N * k)] = bx[i] * by[j] * bz[k];
+  const double* loads[3] = {nullptr, nullptr, nullptr};
+  loads[comp] = L.data();
+  return adi_set_source(P, loads, signal, nsig);
+}
+
+static adi_status run_steps(adi_patch P, int64_t k) {
+  for (int64_t s = 0; s < k; s++) {
+    adi_status st = full_step(P);
+    if (st) return st;
+  }
+  return ADI_OK;
+}
+
+adi_status adi_step(adi_patch P, int64_t k) {
+  CHECK_PATCH(P);
+  if (k < 0) return fail(ADI_ERR_ARG, "adi_step: k < 0");
+  if (!P->have_fields) return fail(ADI_ERR_STATE, "adi_step: fields not set");
+  if (k == 0) return ADI_OK;
+  adi_status st = ADI_OK;
+  if (P->timing) {
+    st = run_steps(P, k);
+  } else {
+    if (!P->graph) {
+      cudaGraph_t g;
+      cudaError_t e = cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal);
+      if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "capture: %s", cudaGetErrorString(e)));
+      const int64_t lc = P->launch_counter;
+      st = full_step(P);
+      P->launch_counter = lc;
+      e = cudaStreamEndCapture(P->stream, &g);
+      if (st) return poison(P, st);
+      if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "capture end: %s", cudaGetErrorString(e)));
+      e = cudaGraphInstantiate(&P->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e)));
+    }
+    for (int64_t s = 0; s < k; s++) {
+      cudaError_t e = cudaGraphLaunch(P->graph, P->stream);
+      if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "graph launch: %s", cudaGetErrorString(e)));
+    }
+    P->launch_counter += k * P->launches_per_step;
+  }
+  if (st) return poison(P, st);
+  P->step_index += k;
+  return ADI_OK;
+}
+
+adi_status adi_synchronize(adi_patch P) {
+  CHECK_PATCH(P);
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "synchronize: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+int64_t adi_step_index(adi_patch P) { return P ? P->step_index : -1; }
+int64_t adi_launches_per_step(adi_patch P) { return P ? P->launches_per_step : -1; }
+void* adi_stream(adi_patch P) { return P ? (void*)P->stream : nullptr; }
+
+adi_status adi_set_timing(adi_patch P, int32_t enable) {
+  CHECK_PATCH(P);
+  cudaStreamSynchronize(P->stream);
+  for (auto& e : P->ev_used) P->ev_free.push_back(e.second.first), P->ev_free.push_back(e.second.second);
+  P->ev_used.clear();
+  for (int c = 0; c < ADI_K_NCLASS; c++) P->t_ms[c] = 0.0, P->t_n[c] = 0;
+  P->timing = enable != 0;
+  return ADI_OK;
+}
+
+adi_status adi_timing_report(adi_patch P, double ms[ADI_K_NCLASS], int64_t launches[ADI_K_NCLASS]) {
+  CHECK_PATCH(P);
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "timing: %s", cudaGetErrorString(e)));
+  for (auto& ev : P->ev_used) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, ev.second.first, ev.second.second);
+    P->t_ms[ev.first] += t;
+    P->t_n[ev.first] += 1;
+    P->ev_free.push_back(ev.second.first);
+    P->ev_free.push_back(ev.second.second);
+  }
+  P->ev_used.clear();
+  for (int c = 0; c < ADI_K_NCLASS; c++) {
+    if (ms) ms[c] = P->t_ms[c];
+    if (launches) launches[c] = P->t_n[c];
+  }
+  return ADI_OK;
+}
+
+// ---- test-only ----------------------------------------------------------------
+adi_status adi_debug_matrices(adi_patch P, double* M, double* S, double* A) {
+  CHECK_PATCH(P);
+  const size_t n = (size_t)P->N * P->N * sizeof(double);
+  if (M) memcpy(M, P->M.data(), n);
+  if (S) memcpy(S, P->S.data(), n);
+  if (A) memcpy(A, P->A.data(), n);
+  return ADI_OK;
+}
+
+adi_status adi_debug_materials_tf(adi_patch P, double* eps_tf, double* mu_tf) {
+  CHECK_PATCH(P);
+  if (eps_tf) cudaMemcpyAsync(eps_tf, P->epsh, P->U * sizeof(double), cudaMemcpyDefault, P->stream);
+  if (mu_tf) cudaMemcpyAsync(mu_tf, P->muh, P->U * sizeof(double), cudaMemcpyDefault, P->stream);
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+static adi_status stage_io_begin(adi_patch P, double** tmp, int ntmp) {
+  for (int i = 0; i < ntmp; i++) {
+    if (cudaMalloc(&tmp[i], P->U * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      for (int j = 0; j < i; j++) cudaFree(tmp[j]);
+      return fail(ADI_ERR_OOM, "debug: cudaMalloc");
+    }
+  }
+  return ADI_OK;
+}
+
+adi_status adi_debug_sweep(adi_patch P, int32_t comp, int32_t axis, int32_t modified, const double* rhs, double* out) {
+  CHECK_PATCH(P);
+  if (comp < 0 || comp > 5 || axis < 0 || axis > 2 || !rhs || !out) return fail(ADI_ERR_ARG, "adi_debug_sweep: bad args");
+  double* t[1];
+  adi_status st = stage_io_begin(P, t, 1);
+  if (st) return st;
+  st = copy_in(P, t[0], rhs, P->U);
+  if (!st) st = sweep(P, comp, axis, modified != 0, t[0], t[0]);
+  if (!st && cudaMemcpyAsync(out, t[0], P->U * sizeof(double), cudaMemcpyDefault, P->stream) != cudaSuccess)
+    st = fail(ADI_ERR_CUDA, "copy out");
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (!st && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e));
+  cudaFree(t[0]);
+  return poison(P, st);
+}
+
+adi_status adi_debug_solve_e(adi_patch P, int32_t s, int32_t d, const double* rhs, double* out) {
+  CHECK_PATCH(P);
+  if ((s != 1 && s != 2) || d < 0 || d > 2 || !rhs || !out) return fail(ADI_ERR_ARG, "adi_debug_solve_e: bad args");
+  double* t[1];
+  adi_status st = stage_io_begin(P, t, 1);
+  if (st) return st;
+  st = copy_in(P, t[0], rhs, P->U);
+  if (!st) st = solve_e(P, s, d, t[0], t[0]);
+  if (!st && cudaMemcpyAsync(out, t[0], P->U * sizeof(double), cudaMemcpyDefault, P->stream) != cudaSuccess)
+    st = fail(ADI_ERR_CUDA, "copy out");
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (!st && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e));
+  cudaFree(t[0]);
+  return poison(P, st);
+}
+
+adi_status adi_debug_rhs_e(adi_patch P, int32_t s, double* const R[3]) {
+  CHECK_PATCH(P);
+  if ((s != 1 && s != 2) || !R) return fail(ADI_ERR_ARG, "adi_debug_rhs_e: bad args");
+  double* t[3];
+  adi_status st = stage_io_begin(P, t, 3);
+  if (st) return st;
+  const double* E[3] = {P->F[0], P->F[1], P->F[2]};
+  const double* H[3] = {P->F[3], P->F[4], P->F[5]};
+  for (int d = 0; d < 3 && !st; d++) st = rhs_e(P, s, d, E, H, t[d]);
+  for (int d = 0; d < 3 && !st; d++)
+    if (R[d] && cudaMemcpyAsync(R[d], t[d], P->U * sizeof(double), cudaMemcpyDefault, P->stream) != cudaSuccess)
+      st = fail(ADI_ERR_CUDA, "copy out");
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (!st && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e));
+  for (int d = 0; d < 3; d++) cudaFree(t[d]);
+  return poison(P, st);
+}
+
+adi_status adi_debug_rhs_h(adi_patch P, int32_t s, const double* const Eo[3], const double* const En[3],
+                           double* const G[3]) {
+  CHECK_PATCH(P);
+  if ((s != 1 && s != 2) || !Eo || !En || !G) return fail(ADI_ERR_ARG, "adi_debug_rhs_h: bad args");
+  double* t[9];
+  adi_status st = stage_io_begin(P, t, 9);
+  if (st) return st;
+  for (int d = 0; d < 3 && !st; d++) {
+    st = copy_in(P, t[d], Eo[d], P->U);
+    if (!st) st = copy_in(P, t[3 + d], En[d], P->U);
+  }
+  const double* eo[3] = {t[0], t[1], t[2]};
+  const double* en[3] = {t[3], t[4], t[5]};
+  for (int d = 0; d < 3 && !st; d++) st = rhs_h(P, s, d, P->F[3 + d], eo, en, t[6 + d]);
+  for (int d = 0; d < 3 && !st; d++)
+    if (G[d] && cudaMemcpyAsync(G[d], t[6 + d], P->U * sizeof(double), cudaMemcpyDefault, P->stream) != cudaSuccess)
+      st = fail(ADI_ERR_CUDA, "copy out");
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (!st && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e));
+  for (int d = 0; d < 9; d++) cudaFree(t[d]);
+  return poison(P, st);
+}
+
+}  // extern "C"

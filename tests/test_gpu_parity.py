@@ -1,0 +1,225 @@
+"""GPU parity: the sm_100a CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerance (BASELINE.json north_star): relative L2 per field <= 1e-10 after all
+steps.  Per-stage checks (matrices, material map, RHS, sweeps) use tighter
+tolerances derived from the arithmetic (fp64 FMA vs -ffp-contract=off,
+different summation order): 1e-13 relative for stencils / maps; for solves
+50 * cond * eps with the fiber condition number.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+import paper_2103_06998_b200 as adi
+
+pytestmark = pytest.mark.gpu
+
+TOL_STEP = 1e-10
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0))
+
+
+def both(n, p, tau, bc=0):
+    return oracle.Patch(n, p, tau, bc), adi.Patch(n, p, tau, bc)
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (3, 2), (8, 2), (5, 3), (4, 4), (3, 5)])
+def test_matrices(n, p):
+    O, G = both(n, p, 0.1)
+    for a, b in zip(O.matrices(), G.matrices()):
+        assert np.allclose(a, b, rtol=1e-13, atol=1e-13 * np.abs(a).max())
+
+
+@pytest.mark.parametrize("n,p", [(3, 1), (6, 2), (5, 3)])
+def test_material_map(n, p):
+    O, G = both(n, p, 0.1)
+    eps = workloads.element_eps(n, "random", seed=n)
+    mu = workloads.element_eps(n, "random", seed=n + 1) / 40.0
+    O.set_materials(eps, mu)
+    G.set_materials(eps, mu)
+    eo, mo = O.get_materials_tf()
+    eg, mg = G.materials_tf()
+    assert rel(eg, eo) <= 1e-14 and rel(mg, mo) <= 1e-14
+
+
+@pytest.mark.parametrize("n,p", [(6, 1), (13, 2), (7, 3), (35, 2)])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_sweeps(n, p, axis):
+    O, G = both(n, p, 0.05)
+    N = n + p
+    eps = workloads.random_tf(N, 3, 1.0, 80.0)
+    O.set_materials_tf(eps)
+    G.set_materials_tf(eps)
+    rng = np.random.default_rng(axis)
+    for comp in (0, 1, 2, 3):
+        rhs = rng.uniform(-1, 1, N ** 3)
+        for mod in (False, True):
+            if comp == 3 and mod:
+                continue
+            ref = O.sweep(comp, axis, mod, rhs)
+            got = G.sweep(comp, axis, mod, rhs)
+            assert rel(got, ref) <= 1e-12, (comp, mod)
+
+
+@pytest.mark.parametrize("n,p", [(5, 1), (9, 2), (6, 3), (34, 2)])
+@pytest.mark.parametrize("s", [1, 2])
+def test_rhs_and_solve(n, p, s):
+    O, G = both(n, p, 0.05)
+    N = n + p
+    eps = workloads.random_tf(N, 5, 1.0, 80.0)
+    mu = workloads.random_tf(N, 6, 0.5, 2.0)
+    O.set_materials_tf(eps, mu)
+    G.set_materials_tf(eps, mu)
+    f = workloads.random_fields(N, 7)
+    O.set_fields(f)
+    G.set_fields(f)
+    Ro, Rg = O.rhs_e(s), G.rhs_e(s)
+    for d in range(3):
+        assert rel(Rg[d], Ro[d]) <= 1e-13, d
+    Eo = O.get_fields()[:3]
+    En = [O.solve_e(s, d, Ro[d]) for d in range(3)]
+    for d in range(3):
+        assert rel(G.solve_e(s, d, Ro[d]), En[d]) <= 1e-12
+    Go, Gg = O.rhs_h(s, Eo, En), G.rhs_h(s, Eo, En)
+    for d in range(3):
+        assert rel(Gg[d], Go[d]) <= 1e-13
+
+
+def _parity_run(n, p, tau, steps, material="uniform", source=None, seed=11, init="random", bc=0):
+    O, G = both(n, p, tau, bc)
+    N = n + p
+    if material != "uniform":
+        eps = workloads.element_eps(n, material)
+        O.set_materials(eps)
+        G.set_materials(eps)
+    if init == "uA":
+        O.project_uA(0.0)
+        f = O.get_fields()
+    else:
+        f = workloads.random_fields(N, seed)
+        O.set_fields(f)
+    G.set_fields(f)
+    if source is not None:
+        sig = workloads.signal(source, tau, steps)
+        pos = workloads.dipole_position(n)
+        J = O.point_load(*pos)
+        O.set_source([None, None, J], sig)
+        G.set_point_source(2, pos, sig)
+    O.step(steps)
+    G.step(steps)
+    fo, fg = O.get_fields(), G.get_fields()
+    errs = [rel(fg[c], fo[c]) for c in range(6)]
+    return errs, fo
+
+
+def test_c1_full():
+    """c1: 8^3, p=2, eps=mu=1, u_A initial data (D10), tau=1e-2, 10 steps."""
+    cfg = workloads.CONFIGS["c1"]
+    errs, _ = _parity_run(cfg["n"], cfg["p"], cfg["tau"], cfg["steps"], init="uA")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_c2_shape_steps():
+    cfg = workloads.CONFIGS["c2"]
+    errs, _ = _parity_run(cfg["n"], cfg["p"], 5e-3, 5, init="uA")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_c3_shape_phantom_source():
+    """p=3, nested-ellipsoid phantom (+/-5% noise) and the Gaussian-pulse dipole (c3 recipe, smaller n)."""
+    errs, fo = _parity_run(16, 3, 1e-2, 40, material="phantom3", source="pulse")
+    assert max(errs) <= TOL_STEP, errs
+    assert max(np.abs(x).max() for x in fo) > 0
+
+
+def test_c4_shape_ragged():
+    """p=2, per-voxel tissue eps in [30,70], modulated-sine dipole; N = 39 (ragged tiles)."""
+    errs, _ = _parity_run(37, 2, 1e-2, 6, material="phantom4", source="modsine")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_natural_bc():
+    errs, _ = _parity_run(6, 2, 0.05, 3, material="random", bc=1)
+    assert max(errs) <= TOL_STEP, errs
+
+
+@pytest.mark.parametrize("p", [1, 4, 5])
+def test_other_degrees(p):
+    errs, _ = _parity_run(4, p, 0.05, 2, material="random")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_single_element():
+    errs, _ = _parity_run(1, 2, 0.1, 3)
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_c4_full_size_one_step():
+    """c4 at full size (128^3, N=130) in the bench launch configuration, one step."""
+    cfg = workloads.CONFIGS["c4"]
+    errs, _ = _parity_run(cfg["n"], cfg["p"], cfg["tau"], 1, material="phantom4", source="modsine")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_step_zero_and_state_errors():
+    G = adi.Patch(4, 2, 0.1)
+    with pytest.raises(adi.AdiError) as e:
+        G.step(1)
+    assert e.value.status == adi.ADI_ERR_STATE
+    f = workloads.random_fields(6, 1)
+    G.set_fields(f)
+    G.step(0)
+    g = G.get_fields()
+    O = oracle.Patch(4, 2, 0.1)
+    O.set_fields(f)
+    for a, b in zip(g, O.get_fields()):
+        assert np.array_equal(a, b)  # PEC zeroing identical, no step taken
+    with pytest.raises(adi.AdiError) as e:
+        G.set_materials(-np.ones(64))
+    assert e.value.status == adi.ADI_ERR_ARG
+    with pytest.raises(adi.AdiError):
+        G.set_materials_tf(np.full(216, np.nan))
+    # failed set_* leaves state intact
+    G.step(1)
+    O.step(1)
+    assert max(rel(a, b) for a, b in zip(G.get_fields(), O.get_fields())) <= TOL_STEP
+
+
+def test_checkpoint_resume_bitwise():
+    f = workloads.random_fields(8, 4)
+    A = adi.Patch(6, 2, 0.05)
+    A.set_materials(workloads.element_eps(6, "random"))
+    A.set_fields(f)
+    A.step(4)
+    B = adi.Patch(6, 2, 0.05)
+    B.set_materials(workloads.element_eps(6, "random"))
+    B.set_fields(f)
+    B.step(2)
+    C = adi.Patch(6, 2, 0.05)
+    C.set_materials(workloads.element_eps(6, "random"))
+    C.set_fields(B.get_fields())
+    C.step(2)
+    for x, y in zip(A.get_fields(), C.get_fields()):
+        assert np.array_equal(x, y)
+
+
+def test_graph_and_direct_paths_agree():
+    f = workloads.random_fields(11, 2)
+    A = adi.Patch(9, 2, 0.05)
+    A.set_fields(f)
+    A.step(3)
+    B = adi.Patch(9, 2, 0.05)
+    B.set_timing(True)
+    B.set_fields(f)
+    B.step(3)
+    rep = B.timing_report()
+    assert rep["sweep_mass"][1] == 3 * 2 * (6 + 9)
+    assert rep["sweep_mod"][1] == 3 * 2 * 3
+    for x, y in zip(A.get_fields(), B.get_fields()):
+        assert np.array_equal(x, y)
