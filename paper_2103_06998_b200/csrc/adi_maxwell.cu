@@ -5,12 +5,15 @@
 // factorisations, material map weights (D6), the per-step launch sequence
 // (SURVEY §8(a) a1-a8), CUDA-graph capture of one step, per-kernel timing.
 // Device side: kernels.cuh.  Nothing here is shared with oracle/.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -156,6 +159,7 @@ struct adi_patch_s {
   adi_status poison = ADI_OK;
   std::vector<double> M, S, A;  // dense host copies
   std::vector<double> wmat;     // material weights N x n (D6)
+  std::vector<double> tab_host; // band tables (host copy)
   double* d_tab = nullptr;      // band tables (4 ops)
   double* d_fac[2] = {nullptr, nullptr};  // mass LU, range variant 0 = [0,N), 1 = [1,N-1)
   double* d_Mb[2] = {nullptr, nullptr};
@@ -181,6 +185,9 @@ struct adi_patch_s {
   int64_t launches_per_step = 0;
   int64_t launch_counter = 0;
   int nsm = 148;
+  int mass_v1 = 0;   // ADI_MASS_V1=1: intermediate-array mass sweep (v1)
+  int mass_bps = 2;  // ADI_MASS_BPS: blocks per SM of the recompute mass sweep
+  int use_tma = 0;   // RHS halo planes by TMA (N even, encoder available; ADI_RHS_CPA=1 disables)
 };
 
 namespace {
@@ -245,102 +252,239 @@ struct LaunchScope {
 };
 
 // ---- launches ---------------------------------------------------------------
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// 3D map of an N^3 fp64 field (x fastest) with a (32+2P) x (16+2P) x 1 box;
+// out-of-bounds elements are zero-filled (the halo outside the patch).
+bool make_field_map(CUtensorMap* m, const double* ptr, int N, int p) {
+  auto enc = tma_encoder();
+  if (!enc || (N & 1)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
+  cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8};
+  cuuint32_t box[3] = {(cuuint32_t)(adi::RT_TX + 2 * p), (cuuint32_t)(adi::RT_TY + 2 * p), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int PP, int KIND, int S, int D>
+void rhs_tma_launch_t(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps) {
+  const int N = P->N;
+  adi::RhsTmaArgs ta;
+  ta.base = args;
+  memcpy(ta.yint, args.zint, sizeof ta.yint);
+  dim3 block(adi::RT_TX, adi::RT_THREADS / adi::RT_TX);
+  dim3 grid((N + adi::RT_TX - 1) / adi::RT_TX, (N + adi::RT_TY - 1) / adi::RT_TY, (N + args.kchunk - 1) / args.kchunk);
+  constexpr size_t smem = adi::rhs_tma_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
+  adi::rhs_tma_kernel<PP, KIND, S, D><<<grid, block, smem, P->stream>>>(maps, ta);
+}
+
+template <int PP, int KIND>
+void rhs_tma_launch_sd(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps, int s, int d) {
+  if (s == 1) {
+    if (d == 0) rhs_tma_launch_t<PP, KIND, 1, 0>(P, args, maps);
+    else if (d == 1) rhs_tma_launch_t<PP, KIND, 1, 1>(P, args, maps);
+    else rhs_tma_launch_t<PP, KIND, 1, 2>(P, args, maps);
+  } else {
+    if (d == 0) rhs_tma_launch_t<PP, KIND, 2, 0>(P, args, maps);
+    else if (d == 1) rhs_tma_launch_t<PP, KIND, 2, 1>(P, args, maps);
+    else rhs_tma_launch_t<PP, KIND, 2, 2>(P, args, maps);
+  }
+}
+
 template <int PP>
-adi_status launch_rhs_p(adi_patch P, const adi::RhsArgs& args, int nt) {
+void rhs_tma_launch_p(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps, int kind, int s, int d) {
+  if (kind == 0) rhs_tma_launch_sd<PP, 0>(P, args, maps, s, d);
+  else rhs_tma_launch_sd<PP, 1>(P, args, maps, s, d);
+}
+
+template <int PP, int KIND, int S, int D>
+cudaError_t rhs_tma_attr_t() {
+  constexpr size_t smem = adi::rhs_tma_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
+  return cudaFuncSetAttribute(adi::rhs_tma_kernel<PP, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int PP>
+cudaError_t rhs_tma_attrs_p() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) { if (x != cudaSuccess) e = x; };
+  acc(rhs_tma_attr_t<PP, 0, 1, 0>()); acc(rhs_tma_attr_t<PP, 0, 1, 1>()); acc(rhs_tma_attr_t<PP, 0, 1, 2>());
+  acc(rhs_tma_attr_t<PP, 0, 2, 0>()); acc(rhs_tma_attr_t<PP, 0, 2, 1>()); acc(rhs_tma_attr_t<PP, 0, 2, 2>());
+  acc(rhs_tma_attr_t<PP, 1, 1, 0>()); acc(rhs_tma_attr_t<PP, 1, 1, 1>()); acc(rhs_tma_attr_t<PP, 1, 1, 2>());
+  acc(rhs_tma_attr_t<PP, 1, 2, 0>()); acc(rhs_tma_attr_t<PP, 1, 2, 1>()); acc(rhs_tma_attr_t<PP, 1, 2, 2>());
+  return e;
+}
+
+cudaError_t rhs_tma_attrs(int p) {
+  switch (p) {
+    case 1: return rhs_tma_attrs_p<1>();
+    case 2: return rhs_tma_attrs_p<2>();
+    case 3: return rhs_tma_attrs_p<3>();
+    case 4: return rhs_tma_attrs_p<4>();
+    case 5: return rhs_tma_attrs_p<5>();
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int PP, int KIND, int S, int D>
+void rhs_launch_t(adi_patch P, const adi::RhsArgs& args) {
   const int N = P->N;
   dim3 block(adi::RHS_TX, adi::RHS_TY);
   dim3 grid((N + adi::RHS_TX - 1) / adi::RHS_TX, (N + adi::RHS_TY - 1) / adi::RHS_TY,
             (N + args.kchunk - 1) / args.kchunk);
-  switch (nt) {
-    case 3: adi::rhs_kernel<PP, 3><<<grid, block, 0, P->stream>>>(args); break;
-    case 4: adi::rhs_kernel<PP, 4><<<grid, block, 0, P->stream>>>(args); break;
-    default: return fail(ADI_ERR_ARG, "rhs: unsupported term count %d", nt);
-  }
-  CUDA_TRY(cudaGetLastError());
-  return ADI_OK;
+  constexpr size_t smem = adi::rhs_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
+  adi::rhs_kernel<PP, KIND, S, D><<<grid, block, smem, P->stream>>>(args);
 }
 
-adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int nt, int comp, int cls) {
+template <int PP, int KIND, int S, int D>
+cudaError_t rhs_attr_t() {
+  constexpr size_t smem = adi::rhs_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
+  return cudaFuncSetAttribute(adi::rhs_kernel<PP, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int PP>
+cudaError_t rhs_attrs_p() {
+  cudaError_t e = cudaSuccess;
+  auto acc = [&](cudaError_t x) { if (x != cudaSuccess) e = x; };
+  acc(rhs_attr_t<PP, 0, 1, 0>()); acc(rhs_attr_t<PP, 0, 1, 1>()); acc(rhs_attr_t<PP, 0, 1, 2>());
+  acc(rhs_attr_t<PP, 0, 2, 0>()); acc(rhs_attr_t<PP, 0, 2, 1>()); acc(rhs_attr_t<PP, 0, 2, 2>());
+  acc(rhs_attr_t<PP, 1, 1, 0>()); acc(rhs_attr_t<PP, 1, 1, 1>()); acc(rhs_attr_t<PP, 1, 1, 2>());
+  acc(rhs_attr_t<PP, 1, 2, 0>()); acc(rhs_attr_t<PP, 1, 2, 1>()); acc(rhs_attr_t<PP, 1, 2, 2>());
+  return e;
+}
+
+cudaError_t rhs_attrs(int p) {
+  switch (p) {
+    case 1: return rhs_attrs_p<1>();
+    case 2: return rhs_attrs_p<2>();
+    case 3: return rhs_attrs_p<3>();
+    case 4: return rhs_attrs_p<4>();
+    case 5: return rhs_attrs_p<5>();
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int PP, int KIND>
+void rhs_launch_sd(adi_patch P, const adi::RhsArgs& args, int s, int d) {
+  if (s == 1) {
+    if (d == 0) rhs_launch_t<PP, KIND, 1, 0>(P, args);
+    else if (d == 1) rhs_launch_t<PP, KIND, 1, 1>(P, args);
+    else rhs_launch_t<PP, KIND, 1, 2>(P, args);
+  } else {
+    if (d == 0) rhs_launch_t<PP, KIND, 2, 0>(P, args);
+    else if (d == 1) rhs_launch_t<PP, KIND, 2, 1>(P, args);
+    else rhs_launch_t<PP, KIND, 2, 2>(P, args);
+  }
+}
+
+template <int PP>
+void rhs_launch_p(adi_patch P, const adi::RhsArgs& args, int kind, int s, int d) {
+  if (kind == 0) rhs_launch_sd<PP, 0>(P, args, s, d);
+  else rhs_launch_sd<PP, 1>(P, args, s, d);
+}
+
+// z-chunk length: enough blocks to fill the machine (>= ~4 waves), halo <= 25%
+int rhs_kchunk(adi_patch P) {
+  const int N = P->N;
+  const int ty = P->use_tma ? adi::RT_TY : adi::RHS_TY;
+  const int64_t tiles = (int64_t)((N + adi::RHS_TX - 1) / adi::RHS_TX) * ((N + ty - 1) / ty);
+  int kc = 64;
+  while (kc > 4 * P->p && tiles * ((N + kc - 1) / kc) < 4LL * P->nsm * 2) kc /= 2;
+  return std::max(kc, 1);
+}
+
+adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp, int cls) {
   args.N = P->N;
-  args.kchunk = P->N <= 96 ? 16 : 64;
+  args.kchunk = rhs_kchunk(P);
   args.tab = P->d_tab;
   args.a = P->a;
   args.b = P->b;
   args.c = P->c;
   args.step = P->d_step;
   for (int ax = 0; ax < 3; ax++) active_range(P, comp, ax, args.lo[ax], args.hi[ax]);
-  LaunchScope ls(P, cls);
-  switch (P->p) {
-    case 1: return launch_rhs_p<1>(P, args, nt);
-    case 2: return launch_rhs_p<2>(P, args, nt);
-    case 3: return launch_rhs_p<3>(P, args, nt);
-    case 4: return launch_rhs_p<4>(P, args, nt);
-    case 5: return launch_rhs_p<5>(P, args, nt);
+  // interior Toeplitz stencils (row N/2 of M, A, B; identical for rows 2P..N-2P-1)
+  {
+    const int W = P->W, r = P->N / 2;
+    for (int o = 0; o < 3; o++)
+      for (int q = 0; q < 11; q++) args.zint[o][q] = q < W ? P->tab_host[((size_t)o * P->N + r) * W + q] : 0.0;
   }
-  return fail(ADI_ERR_ARG, "rhs: bad p");
+  LaunchScope ls(P, cls);
+  const int d = comp % 3;
+  if (P->use_tma) {
+    adi::RhsTmaMaps maps;
+    const int nt = kind == 0 ? 4 : 3;
+    bool ok = true;
+    for (int t = 0; t < nt; t++) ok = ok && make_field_map(&maps.m[t], args.u[t], P->N, P->p);
+    if (ok) {
+      switch (P->p) {
+        case 1: rhs_tma_launch_p<1>(P, args, maps, kind, s, d); break;
+        case 2: rhs_tma_launch_p<2>(P, args, maps, kind, s, d); break;
+        case 3: rhs_tma_launch_p<3>(P, args, maps, kind, s, d); break;
+        case 4: rhs_tma_launch_p<4>(P, args, maps, kind, s, d); break;
+        case 5: rhs_tma_launch_p<5>(P, args, maps, kind, s, d); break;
+      }
+      CUDA_TRY(cudaGetLastError());
+      return ADI_OK;
+    }
+  }
+  switch (P->p) {
+    case 1: rhs_launch_p<1>(P, args, kind, s, d); break;
+    case 2: rhs_launch_p<2>(P, args, kind, s, d); break;
+    case 3: rhs_launch_p<3>(P, args, kind, s, d); break;
+    case 4: rhs_launch_p<4>(P, args, kind, s, d); break;
+    case 5: rhs_launch_p<5>(P, args, kind, s, d); break;
+    default: return fail(ADI_ERR_ARG, "rhs: bad p");
+  }
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
 }
 
-adi::RhsTerm term(const double* u, int ox, int oy, int oz, int scale, double sign) {
-  adi::RhsTerm t;
-  t.u = u;
-  t.op[0] = ox;
-  t.op[1] = oy;
-  t.op[2] = oz;
-  t.scale = scale;
-  t.sign = sign;
-  return t;
-}
-
-// Operator triple with A on axis `ax` and M elsewhere.
-void deriv_ops(int ax, int op[3]) {
-  for (int k = 0; k < 3; k++) op[k] = (k == ax) ? adi::OP_A : adi::OP_M;
-}
-
-// RHS of the E system of component d, substep s (a1/a5):
-//   R_d = M^3 E_d + a [ d_{d+1} H_{d+2} - d_{d+2} H_{d+1} ] + c (A on d, B on sigma) E_sigma
-// with sigma the stiffened axis (discrete1/discrete3; dupa1ab P:373-386).
+// RHS of the E system of component d, substep s (a1/a5); term inputs in the order
+// of adi::RhsProg<0,s,d>: E_d, H_{d+2}, H_{d+1}, E_sigma.
 adi_status rhs_e(adi_patch P, int s, int d, const double* const E[3], const double* const H[3], double* out) {
   adi::RhsArgs args{};
-  int op[3];
-  args.term[0] = term(E[d], adi::OP_M, adi::OP_M, adi::OP_M, adi::SC_ONE, 1.0);
-  deriv_ops((d + 1) % 3, op);
-  args.term[1] = term(H[(d + 2) % 3], op[0], op[1], op[2], adi::SC_A, 1.0);
-  deriv_ops((d + 2) % 3, op);
-  args.term[2] = term(H[(d + 1) % 3], op[0], op[1], op[2], adi::SC_A, -1.0);
-  const int sg = stiff_axis(s, d);
-  int rop[3];
-  for (int k = 0; k < 3; k++) rop[k] = adi::OP_M;
-  rop[d] = adi::OP_A;
-  rop[sg] = adi::OP_B;
-  args.term[3] = term(E[sg], rop[0], rop[1], rop[2], adi::SC_C, 1.0);
+  args.u[0] = E[d];
+  args.u[1] = H[(d + 2) % 3];
+  args.u[2] = H[(d + 1) % 3];
+  args.u[3] = E[stiff_axis(s, d)];
   args.load = P->load[d];
   args.signal = P->signal;
   args.nsig = P->nsig;
   args.out = out;
-  return launch_rhs(P, args, 4, d, ADI_K_RHS_E);
+  return launch_rhs(P, args, 0, s, d, ADI_K_RHS_E);
 }
 
-// RHS of the H system of component d, substep s (a3/a7):
-//   s=1: G_d = M^3 H_d - b d_{d+1} Eo_{d+2} + b d_{d+2} En_{d+1}   (discrete2)
-//   s=2: G_d = M^3 H_d + b d_{d+2} Eo_{d+1} - b d_{d+1} En_{d+2}   (discrete4 with D2)
+// RHS of the H system of component d, substep s (a3/a7); inputs of adi::RhsProg<1,s,d>.
 adi_status rhs_h(adi_patch P, int s, int d, const double* Hd, const double* const Eo[3], const double* const En[3],
                  double* out) {
   adi::RhsArgs args{};
-  int op[3];
-  args.term[0] = term(Hd, adi::OP_M, adi::OP_M, adi::OP_M, adi::SC_ONE, 1.0);
+  args.u[0] = Hd;
   if (s == 1) {
-    deriv_ops((d + 1) % 3, op);
-    args.term[1] = term(Eo[(d + 2) % 3], op[0], op[1], op[2], adi::SC_B, -1.0);
-    deriv_ops((d + 2) % 3, op);
-    args.term[2] = term(En[(d + 1) % 3], op[0], op[1], op[2], adi::SC_B, 1.0);
+    args.u[1] = Eo[(d + 2) % 3];
+    args.u[2] = En[(d + 1) % 3];
   } else {
-    deriv_ops((d + 2) % 3, op);
-    args.term[1] = term(Eo[(d + 1) % 3], op[0], op[1], op[2], adi::SC_B, 1.0);
-    deriv_ops((d + 1) % 3, op);
-    args.term[2] = term(En[(d + 2) % 3], op[0], op[1], op[2], adi::SC_B, -1.0);
+    args.u[1] = Eo[(d + 1) % 3];
+    args.u[2] = En[(d + 2) % 3];
   }
   args.out = out;
-  return launch_rhs(P, args, 3, 3 + d, ADI_K_RHS_H);
+  return launch_rhs(P, args, 1, s, 3 + d, ADI_K_RHS_H);
 }
 
 int64_t ntiles_axis(int N, int axis) {
@@ -361,10 +505,17 @@ adi_status launch_sweep_p(adi_patch P, const adi::SweepArgs& A, bool modified) {
     constexpr int CH = 16;
     auto k = adi::sweep_mod_kernel<PP, CH>;
     k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
-  } else {
+  } else if (P->mass_v1) {
     constexpr int CH = 32;
     auto k = adi::sweep_mass_kernel<PP, CH>;
     k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
+  } else {
+    constexpr int CH = 32;
+    const int nck = (P->N + CH - 1) / CH;
+    size_t smem2 = ((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * nck * PP * 32) * sizeof(double);
+    if (A.axis == 0) smem2 += (size_t)adi::SWEEP_WARPS * 32 * 33 * sizeof(double);
+    const int64_t grid2 = std::min<int64_t>(blocks_needed, (int64_t)nsm * P->mass_bps);
+    adi::sweep_mass2_kernel<PP, CH><<<(unsigned)grid2, 32 * adi::SWEEP_WARPS, smem2, P->stream>>>(A, nck);
   }
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
@@ -377,6 +528,10 @@ adi_status sweep_attrs_p(adi_patch P) {
   const int mod = (int)(((size_t)2 * P->N * W + (size_t)adi::SWEEP_WARPS * 32 * 33) * sizeof(double));
   CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mass_kernel<PP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass));
   CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mod_kernel<PP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mod));
+  const int nck = (P->N + 31) / 32;
+  const int mass2 = (int)(((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * nck * PP * 32 + (size_t)adi::SWEEP_WARPS * 32 * 33) *
+                          sizeof(double));
+  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mass2_kernel<PP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass2));
   return ADI_OK;
 }
 
@@ -666,7 +821,19 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   }
   const int N = P->N, p = P->p, W = P->W;
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (const char* s = getenv("ADI_MASS_V1")) P->mass_v1 = atoi(s);
+  if (const char* s = getenv("ADI_MASS_BPS")) P->mass_bps = std::max(1, atoi(s));
   if (sweep_attrs(P)) return bail(fail(ADI_ERR_ARG, "N = %d too large for the sweep kernels' shared memory", N));
+  if (rhs_attrs(p) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
+  {
+    const char* s = getenv("ADI_RHS_CPA");
+    // TMA boxes no larger than the tensor (small patches use the cp.async kernel)
+    P->use_tma = (N % 2 == 0) && N >= adi::RT_TX + 2 * p && tma_encoder() != nullptr && !(s && atoi(s));
+    if (P->use_tma && rhs_tma_attrs(p) != cudaSuccess) {
+      cudaGetLastError();
+      P->use_tma = 0;
+    }
+  }
   Space1D sp(P->n, p);
   assemble_1d(sp, P->M, P->S, P->A);
   // material weights (D6): w[r*n+e] = int_{elem e} B_r / int B_r (Gauss q = p+1, exact)
@@ -701,6 +868,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     }
     return true;
   };
+  P->tab_host = tab;
   if (!dmalloc(&P->d_tab, tab.size())) return bail(fail(ADI_ERR_OOM, "cudaMalloc band tables"));
   cudaMemcpy(P->d_tab, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice);
   for (int var = 0; var < 2; var++) {

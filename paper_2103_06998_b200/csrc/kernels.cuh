@@ -12,6 +12,7 @@
 //                    per fiber, no pivoting -- D12), one fiber per lane.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace adi {
@@ -23,20 +24,50 @@ enum Scale { SC_ONE = 0, SC_A = 1, SC_C = 2, SC_B = 3 };
 
 constexpr int RHS_TX = 32;
 constexpr int RHS_TY = 8;
+constexpr int RHS_THREADS = RHS_TX * RHS_TY;
 constexpr int RHS_MAXT = 4;
 
-struct RhsTerm {
-  const double* u;  // input field (N^3)
-  int op[3];        // x, y, z operator codes
-  int scale;        // Scale
-  double sign;      // +1 / -1
+// The right-hand sides as compile-time "programs" of row-scaled Kronecker terms.
+// KIND 0 = E system of component D in substep S (a1/a5):
+//   R_D = M^3 E_D + a [ d_{D+1} H_{D+2} - d_{D+2} H_{D+1} ] + c (A on D, B on sigma) E_sigma,
+//   sigma = stiffened axis ((D+1)%3 in substep 1, (D+2)%3 in substep 2; K1/K2 of P:250-251);
+//   (discrete1/discrete3 P:235/241; expanded in dupa1ab P:373-386).
+// KIND 1 = H system of component D (a3/a7):
+//   S=1: G_D = M^3 H_D - b d_{D+1} Eo_{D+2} + b d_{D+2} En_{D+1}   (discrete2 P:238, C1/C2 P:254-255 + D3)
+//   S=2: G_D = M^3 H_D + b d_{D+2} Eo_{D+1} - b d_{D+1} En_{D+2}   (discrete4 P:244 with the sign D2)
+// "d_a" is the advection matrix A (derivative on the trial function, D4) on axis a.
+template <int KIND, int S, int D>
+struct RhsProg {
+  static constexpr int NT = KIND == 0 ? 4 : 3;
+  static constexpr int SIG = S == 1 ? (D + 1) % 3 : (D + 2) % 3;
+  __host__ __device__ static constexpr int op(int t, int ax) {
+    return t == 0 ? OP_M
+         : KIND == 0 ? (t == 1 ? (ax == (D + 1) % 3 ? OP_A : OP_M)
+                      : t == 2 ? (ax == (D + 2) % 3 ? OP_A : OP_M)
+                               : (ax == D ? OP_A : ax == SIG ? OP_B : OP_M))
+         : S == 1 ? (t == 1 ? (ax == (D + 1) % 3 ? OP_A : OP_M) : (ax == (D + 2) % 3 ? OP_A : OP_M))
+                  : (t == 1 ? (ax == (D + 2) % 3 ? OP_A : OP_M) : (ax == (D + 1) % 3 ? OP_A : OP_M));
+  }
+  __host__ __device__ static constexpr int scale(int t) {
+    return t == 0 ? SC_ONE : KIND == 0 ? (t == 3 ? SC_C : SC_A) : SC_B;
+  }
+  __host__ __device__ static constexpr double sign(int t) {
+    return t == 0 ? 1.0
+         : KIND == 0 ? (t == 2 ? -1.0 : 1.0)
+         : S == 1 ? (t == 1 ? -1.0 : 1.0) : (t == 1 ? 1.0 : -1.0);
+  }
 };
+
+template <int P, int NT>
+constexpr size_t rhs_smem_bytes() {
+  return sizeof(double) * (3 * NT * (RHS_TY + 2 * P) * (RHS_TX + 2 * P) + NT * (RHS_TY + 2 * P) * RHS_TX);
+}
 
 struct RhsArgs {
   int N;
   int kchunk;            // z-planes per block
   const double* tab;     // band tables, 4 ops
-  RhsTerm term[RHS_MAXT];
+  const double* u[RHS_MAXT];  // term inputs
   const double* a;       // tau/(2 eps^)
   const double* b;       // tau/(2 mu^)
   const double* c;       // tau^2/(4 eps^ mu^)
@@ -45,19 +76,39 @@ struct RhsArgs {
   const int64_t* step;   // device step counter
   int64_t nsig;
   int lo[3], hi[3];      // active ranges of the output component (PEC, D1)
+  double zint[3][11];    // interior (Toeplitz) stencils of M, A, B (rows 2P..N-2P-1)
   double* out;
 };
 
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int sz = valid ? 8 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // out[I] = sum_t sign_t * scale_t[I] * ((X_t (x) Y_t (x) Z_t) u_t)[I]  (- a s J),
-// zero outside the active set.
-template <int P, int NT>
-__global__ void __launch_bounds__(RHS_TX * RHS_TY)
+// zero outside the active set.  One block = a 32 x 8 xy tile streaming a z-chunk.
+// Input planes (with a P-wide halo) arrive in a 3-deep shared-memory ring by
+// cp.async (two planes in flight); the x-pass goes shared -> shared, the y-pass
+// shared -> a (2P+1)-plane register window per term (rotating slots, unrolled by
+// 2P+1 so no register moves), the z-pass + row scaling run on the window with the
+// Toeplitz interior stencil from the constant bank (boundary rows from the table).
+template <int P, int KIND, int S, int D>
+__global__ void __launch_bounds__(RHS_THREADS, (P <= 2 ? 2 : 1))
 rhs_kernel(const RhsArgs args) {
+  using Prog = RhsProg<KIND, S, D>;
+  constexpr int NT = Prog::NT;
   constexpr int W = 2 * P + 1;
   constexpr int HX = RHS_TX + 2 * P;
   constexpr int HY = RHS_TY + 2 * P;
-  __shared__ double s_in[NT][HY][HX];
-  __shared__ double s_x[NT][HY][RHS_TX];
+  constexpr int PLANE = HY * HX;
+  constexpr int PFT = (PLANE + RHS_THREADS - 1) / RHS_THREADS;  // copies per term per thread
+  extern __shared__ double rhs_smem[];
+  double* s_ring = rhs_smem;                                   // [3][NT][PLANE]
+  double(*s_x)[HY][RHS_TX] = reinterpret_cast<double(*)[HY][RHS_TX]>(rhs_smem + 3 * NT * PLANE);
 
   const int N = args.N;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -68,79 +119,352 @@ rhs_kernel(const RhsArgs args) {
   const int i = i0 + tx, j = j0 + ty;
   const int64_t NN = (int64_t)N * N;
 
-  double cx[NT][W], cy[NT][W], w[NT][W];
+  // per-thread coefficient rows of the three operator kinds (dead ones are eliminated)
+  double cx[3][W], cy[3][W];
 #pragma unroll
-  for (int t = 0; t < NT; t++) {
+  for (int o = 0; o < 3; o++)
 #pragma unroll
     for (int q = 0; q < W; q++) {
-      cx[t][q] = (i < N) ? args.tab[((int64_t)args.term[t].op[0] * N + i) * W + q] : 0.0;
-      cy[t][q] = (j < N) ? args.tab[((int64_t)args.term[t].op[1] * N + j) * W + q] : 0.0;
-      w[t][q] = 0.0;
+      cx[o][q] = (i < N) ? __ldg(args.tab + ((int64_t)o * N + i) * W + q) : 0.0;
+      cy[o][q] = (j < N) ? __ldg(args.tab + ((int64_t)o * N + j) * W + q) : 0.0;
     }
+  // this thread's copy slots inside a halo plane (same for every term and plane)
+  int coff[PFT];
+  bool cval[PFT], cin[PFT];
+#pragma unroll
+  for (int f = 0; f < PFT; f++) {
+    const int e = tid + f * RHS_THREADS;
+    cin[f] = e < PLANE;
+    const int yy = e / HX, xx = e - yy * HX;
+    const int gi = i0 - P + xx, gj = j0 - P + yy;
+    cval[f] = cin[f] && gi >= 0 && gi < N && gj >= 0 && gj < N;
+    coff[f] = cval[f] ? gi + N * gj : 0;
   }
+  auto issue = [&](int kin) {
+    if (kin >= k1 + P) {  // nothing left: an empty group keeps the wait_group arithmetic uniform
+      cp_async_commit();
+      return;
+    }
+    const int slot = ((kin - (k0 - P)) % 3) * NT * PLANE;
+    const bool kok = kin >= 0 && kin < N;
+    const int64_t pb = kok ? NN * kin : 0;
+#pragma unroll
+    for (int t = 0; t < NT; t++) {
+      const double* base = args.u[t] + pb;
+#pragma unroll
+      for (int f = 0; f < PFT; f++)
+        if (cin[f]) cp_async8(s_ring + slot + t * PLANE + tid + f * RHS_THREADS, base + coff[f], kok && cval[f]);
+    }
+    cp_async_commit();
+  };
+
+  double w[NT][W];
+#pragma unroll
+  for (int t = 0; t < NT; t++)
+#pragma unroll
+    for (int q = 0; q < W; q++) w[t][q] = 0.0;
   double sval = 0.0;
-  if (args.load != nullptr && args.signal != nullptr) {
+  if (KIND == 0 && args.load != nullptr && args.signal != nullptr) {
     const int64_t s = *args.step;
     if (s < args.nsig) sval = args.signal[s];
   }
 
-  for (int kin = k0 - P; kin < k1 + P; kin++) {
-    __syncthreads();
-    const bool kok = (kin >= 0 && kin < N);
+  const int kbeg = k0 - P, kend = k1 + P;  // input planes [kbeg, kend)
+  issue(kbeg);
+  issue(kbeg + 1);
+  for (int g0 = kbeg; g0 < kend; g0 += W) {
 #pragma unroll
-    for (int t = 0; t < NT; t++) {
-      const double* __restrict__ u = args.term[t].u;
-      for (int idx = tid; idx < HY * HX; idx += RHS_TX * RHS_TY) {
-        const int yy = idx / HX, xx = idx - yy * HX;
-        const int gi = i0 - P + xx, gj = j0 - P + yy;
-        double v = 0.0;
-        if (kok && gi >= 0 && gi < N && gj >= 0 && gj < N) v = __ldg(u + gi + (int64_t)N * gj + NN * kin);
-        s_in[t][yy][xx] = v;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < NT; t++) {
-      for (int yy = ty; yy < HY; yy += RHS_TY) {
-        double acc = 0.0;
-#pragma unroll
-        for (int q = 0; q < W; q++) acc = fma(cx[t][q], s_in[t][yy][tx + q], acc);
-        s_x[t][yy][tx] = acc;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < NT; t++) {
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < W; q++) acc = fma(cy[t][q], s_x[t][ty + q][tx], acc);
-#pragma unroll
-      for (int q = 0; q < W - 1; q++) w[t][q] = w[t][q + 1];
-      w[t][W - 1] = acc;
-    }
-    const int k = kin - P;
-    if (k >= k0 && k < k1 && i < N && j < N) {
-      const int64_t I = i + (int64_t)N * j + NN * k;
-      const bool active = i >= args.lo[0] && i < args.hi[0] && j >= args.lo[1] && j < args.hi[1] &&
-                          k >= args.lo[2] && k < args.hi[2];
-      double val = 0.0;
-      if (active) {
+    for (int ph = 0; ph < W; ph++) {
+      const int kin = g0 + ph;
+      if (kin < kend) {
+        cp_async_wait<1>();
+        __syncthreads();  // plane kin visible to all; s_x free; ring slot of kin-1 free
+        issue(kin + 2);  // keep two planes in flight
+        const double* ring = s_ring + ((kin - kbeg) % 3) * NT * PLANE;
 #pragma unroll
         for (int t = 0; t < NT; t++) {
-          const double* zc = args.tab + ((int64_t)args.term[t].op[2] * N + k) * W;
-          double z = 0.0;
+          for (int yy = ty; yy < HY; yy += RHS_TY) {
+            double acc = 0.0;
+            const double* row = ring + t * PLANE + yy * HX + tx;
 #pragma unroll
-          for (int q = 0; q < W; q++) z = fma(__ldg(zc + q), w[t][q], z);
-          double sc = 1.0;
-          const int kind = args.term[t].scale;
-          if (kind == SC_A) sc = args.a[I];
-          else if (kind == SC_C) sc = args.c[I];
-          else if (kind == SC_B) sc = args.b[I];
-          val = fma(args.term[t].sign * sc, z, val);
+            for (int q = 0; q < W; q++) acc = fma(cx[Prog::op(t, 0)][q], row[q], acc);
+            s_x[t][yy][tx] = acc;
+          }
         }
-        if (sval != 0.0) val -= args.a[I] * sval * args.load[I];
+        __syncthreads();  // s_x complete
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < W; q++) acc = fma(cy[Prog::op(t, 1)][q], s_x[t][ty + q][tx], acc);
+          w[t][ph] = acc;  // slot of plane kin = (kin - kbeg) % W = ph
+        }
+        const int k = kin - P;
+        if (k >= k0 && i < N && j < N) {
+          const int64_t I = i + (int64_t)N * j + NN * k;
+          const bool active = i >= args.lo[0] && i < args.hi[0] && j >= args.lo[1] && j < args.hi[1] &&
+                              k >= args.lo[2] && k < args.hi[2];
+          double val = 0.0;
+          if (active) {
+            // plane k-P+q sits in slot (ph + 1 + q) % W
+            double zs[3] = {0.0, 0.0, 0.0};  // scale groups: one, a|b, c
+            const bool zin = k >= 2 * P && k < N - 2 * P;
+#pragma unroll
+            for (int t = 0; t < NT; t++) {
+              const int zop = Prog::op(t, 2);
+              double z = 0.0;
+              if (zin) {
+#pragma unroll
+                for (int q = 0; q < W; q++) z = fma(args.zint[zop][q], w[t][(ph + 1 + q) % W], z);
+              } else {
+                const double* zc = args.tab + ((int64_t)zop * N + k) * W;
+#pragma unroll
+                for (int q = 0; q < W; q++) z = fma(__ldg(zc + q), w[t][(ph + 1 + q) % W], z);
+              }
+              const int grp = Prog::scale(t) == SC_ONE ? 0 : Prog::scale(t) == SC_C ? 2 : 1;
+              zs[grp] = fma(Prog::sign(t), z, zs[grp]);
+            }
+            if (KIND == 0) {
+              const double av = args.a[I];
+              val = zs[0] + av * zs[1] + args.c[I] * zs[2];
+              if (sval != 0.0) val -= av * sval * args.load[I];
+            } else {
+              val = zs[0] + args.b[I] * zs[1];
+            }
+          }
+          args.out[I] = val;
+        }
       }
-      args.out[I] = val;
+    }
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// RHS, TMA variant (N even): the halo planes arrive by one cp.async.bulk.tensor
+// per term per plane (zero fill out of bounds = the halo outside the patch),
+// tracked by mbarriers in a 3-stage ring; a thread owns two y-rows (register
+// tiling of the y-pass); x-pass output is double-buffered so each plane needs a
+// single __syncthreads.
+// ---------------------------------------------------------------------------
+constexpr int RT_TX = 32;
+constexpr int RT_TY = 16;
+constexpr int RT_THREADS = 256;  // 32 x 8, two rows each
+
+struct RhsTmaMaps {
+  CUtensorMap m[RHS_MAXT];
+};
+
+struct RhsTmaArgs {
+  RhsArgs base;
+  double yint[3][11];  // interior stencils (same as base.zint) for the y-pass of interior tiles
+};
+
+template <int P>
+struct RtGeom {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int HX = RT_TX + 2 * P;
+  static constexpr int HY = RT_TY + 2 * P;
+  static constexpr int PLANE = HX * HY;
+  static constexpr int PLANEP = (PLANE + 15) / 16 * 16;  // 128-byte aligned stage slices
+};
+
+template <int P, int NT>
+constexpr size_t rhs_tma_smem_bytes() {
+  using G = RtGeom<P>;
+  return sizeof(double) * (3 * NT * G::PLANEP + 2 * NT * G::HY * RT_TX + 3 * RT_TY * G::W) + 3 * sizeof(uint64_t) + 128;
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int P, int KIND, int S, int D>
+__global__ void __launch_bounds__(RT_THREADS, 2)
+rhs_tma_kernel(const __grid_constant__ RhsTmaMaps maps, const __grid_constant__ RhsTmaArgs targs) {
+  using Prog = RhsProg<KIND, S, D>;
+  using G = RtGeom<P>;
+  constexpr int NT = Prog::NT;
+  constexpr int W = G::W, HX = G::HX, HY = G::HY, PLANEP = G::PLANEP;
+  const RhsArgs& args = targs.base;
+  extern __shared__ __align__(128) double rt_smem_raw[];
+  double* rt_smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(rt_smem_raw) + 127) & ~uintptr_t(127));
+  double* ring = rt_smem;                                              // [3][NT][PLANEP]
+  double* sx = rt_smem + 3 * NT * PLANEP;                              // [2][NT][HY][TX]
+  double* scy = sx + 2 * NT * HY * RT_TX;                              // [3 ops][TY][W] (boundary tiles)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(scy + 3 * RT_TY * W);    // [3]
+
+  const int N = args.N;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // ty in [0,8): rows 2ty, 2ty+1
+  const int i0 = blockIdx.x * RT_TX, j0 = blockIdx.y * RT_TY;
+  const int k0 = blockIdx.z * args.kchunk;
+  const int k1 = min(N, k0 + args.kchunk);
+  const int i = i0 + tx;
+  const int jA = j0 + 2 * ty, jB = jA + 1;
+  const int64_t NN = (int64_t)N * N;
+  const int kbeg = k0 - P, kend = k1 + P;
+  const bool yint_tile = (j0 >= 2 * P) && (j0 + RT_TY <= N - 2 * P);
+
+  if (tx == 0 && ty == 0) {
+    for (int s = 0; s < 3; s++) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (!yint_tile) {
+    const int tid = ty * RT_TX + tx;
+    for (int e = tid; e < 3 * RT_TY * W; e += RT_THREADS) {
+      const int o = e / (RT_TY * W), rem = e - o * (RT_TY * W), r = rem / W, q = rem - r * W;
+      const int jj = j0 + r;
+      scy[e] = (jj < N) ? args.tab[((int64_t)o * N + jj) * W + q] : 0.0;
+    }
+  }
+  __syncthreads();
+
+  auto produce = [&](int kin) {  // called by thread (0,0) only
+    if (kin >= kend) return;
+    const int st = (kin - kbeg) % 3;
+    mbar_expect_tx(&bar[st], (unsigned)(NT * HX * HY * sizeof(double)));
+#pragma unroll
+    for (int t = 0; t < NT; t++) tma_load_3d(ring + (st * NT + t) * PLANEP, &maps.m[t], i0 - P, j0 - P, kin, &bar[st]);
+  };
+  if (tx == 0 && ty == 0) {
+    produce(kbeg);
+    produce(kbeg + 1);
+    produce(kbeg + 2);
+  }
+
+  double cx[3][W];
+#pragma unroll
+  for (int o = 0; o < 3; o++)
+#pragma unroll
+    for (int q = 0; q < W; q++) cx[o][q] = (i < N) ? __ldg(args.tab + ((int64_t)o * N + i) * W + q) : 0.0;
+  double w[NT][2][W];
+#pragma unroll
+  for (int t = 0; t < NT; t++)
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+      for (int q = 0; q < W; q++) w[t][r][q] = 0.0;
+  double sval = 0.0;
+  if (KIND == 0 && args.load != nullptr && args.signal != nullptr) {
+    const int64_t s = *args.step;
+    if (s < args.nsig) sval = args.signal[s];
+  }
+
+  for (int g0 = kbeg; g0 < kend; g0 += W) {
+#pragma unroll
+    for (int ph = 0; ph < W; ph++) {
+      const int kin = g0 + ph;
+      if (kin < kend) {
+        const int it = kin - kbeg;
+        const int st = it % 3;
+        double* sxb = sx + (it & 1) * NT * HY * RT_TX;
+        mbar_wait(&bar[st], (unsigned)((it / 3) & 1));
+        // x-pass: rows yy = ty, ty+8, ty+16 ...
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          const double* pl = ring + (st * NT + t) * PLANEP;
+#pragma unroll
+          for (int yy0 = 0; yy0 < HY; yy0 += 8) {
+            const int yy = yy0 + ty;
+            if (yy < HY) {
+              const double* row = pl + yy * HX + tx;
+              double acc = 0.0;
+#pragma unroll
+              for (int q = 0; q < W; q++) acc = fma(cx[Prog::op(t, 0)][q], row[q], acc);
+              sxb[(t * HY + yy) * RT_TX + tx] = acc;
+            }
+          }
+        }
+        __syncthreads();  // x-pass(kin) visible; ring stage st free; (y-pass(kin-1) used the other sx buffer)
+        if (tx == 0 && ty == 0) produce(kin + 3);
+        // y-pass: outputs rows 2ty, 2ty+1 of the tile
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          double col[W + 1];
+#pragma unroll
+          for (int q = 0; q <= W; q++) col[q] = sxb[(t * HY + 2 * ty + q) * RT_TX + tx];
+          double vA = 0.0, vB = 0.0;
+          const int yop = Prog::op(t, 1);
+          if (yint_tile) {
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+              vA = fma(targs.yint[yop][q], col[q], vA);
+              vB = fma(targs.yint[yop][q], col[q + 1], vB);
+            }
+          } else {
+            const double* cA = scy + (yop * RT_TY + 2 * ty) * W;
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+              vA = fma(cA[q], col[q], vA);
+              vB = fma(cA[W + q], col[q + 1], vB);
+            }
+          }
+          w[t][0][ph] = vA;
+          w[t][1][ph] = vB;
+        }
+        const int k = kin - P;
+        if (k >= k0 && i < N) {
+          const bool zin = k >= 2 * P && k < N - 2 * P;
+          const bool ak = k >= args.lo[2] && k < args.hi[2] && i >= args.lo[0] && i < args.hi[0];
+#pragma unroll
+          for (int r = 0; r < 2; r++) {
+            const int j = r == 0 ? jA : jB;
+            if (j < N) {
+              const int64_t I = i + (int64_t)N * j + NN * k;
+              double val = 0.0;
+              if (ak && j >= args.lo[1] && j < args.hi[1]) {
+                double zs[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int t = 0; t < NT; t++) {
+                  const int zop = Prog::op(t, 2);
+                  double z = 0.0;
+                  if (zin) {
+#pragma unroll
+                    for (int q = 0; q < W; q++) z = fma(args.zint[zop][q], w[t][r][(ph + 1 + q) % W], z);
+                  } else {
+                    const double* zc = args.tab + ((int64_t)zop * N + k) * W;
+#pragma unroll
+                    for (int q = 0; q < W; q++) z = fma(__ldg(zc + q), w[t][r][(ph + 1 + q) % W], z);
+                  }
+                  const int grp = Prog::scale(t) == SC_ONE ? 0 : Prog::scale(t) == SC_C ? 2 : 1;
+                  zs[grp] = fma(Prog::sign(t), z, zs[grp]);
+                }
+                if (KIND == 0) {
+                  const double av = args.a[I];
+                  val = zs[0] + av * zs[1] + args.c[I] * zs[2];
+                  if (sval != 0.0) val -= av * sval * args.load[I];
+                } else {
+                  val = zs[0] + args.b[I] * zs[1];
+                }
+              }
+              args.out[I] = val;
+            }
+          }
+        }
+      }
     }
   }
 }
@@ -320,6 +644,150 @@ sweep_mass_kernel(const SweepArgs A) {
         }
       }
       store_rows<CH>(A, A.out, tile, lane, base, stride, valid, c0, T, v);
+    }
+  }
+}
+
+// Raw (un-transposed) loads of rows [c0, c0+CH) of the warp's 32 fibers into
+// registers; finish_rows() turns them into v[r] = row c0+r of this lane's fiber.
+// Splitting issue and finish lets a chunk's loads fly while the previous chunk
+// is being eliminated (x-axis fibers go through the per-warp smem transpose).
+template <int CH>
+__device__ __forceinline__ void issue_rows(const SweepArgs& A, const double* __restrict__ src, int tile, int lane,
+                                           int64_t base, int64_t stride, bool valid, int c0, double* raw) {
+  if (A.axis != 0) {
+#pragma unroll
+    for (int r = 0; r < CH; r++) {
+      const int row = c0 + r;
+      raw[r] = (valid && row < A.hi) ? __ldg(src + base + (int64_t)row * stride) : 0.0;
+    }
+  } else {
+    const int64_t NN = (int64_t)A.N * A.N;
+    const int64_t f0 = (int64_t)tile * 32;
+    const int row = c0 + lane;
+#pragma unroll
+    for (int r = 0; r < CH; r++) {  // CH == 32 for the x axis
+      raw[r] = (f0 + r < NN && row < A.hi) ? __ldg(src + (int64_t)A.N * (f0 + r) + row) : 0.0;
+    }
+  }
+}
+
+template <int CH>
+__device__ __forceinline__ void finish_rows(const SweepArgs& A, int lane, double (*T)[33], const double* raw,
+                                            double* v) {
+  if (A.axis != 0) {
+#pragma unroll
+    for (int r = 0; r < CH; r++) v[r] = raw[r];
+  } else {
+#pragma unroll
+    for (int r = 0; r < CH; r++) T[r][lane] = raw[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < CH; r++) v[r] = T[lane][r];
+    __syncwarp();
+  }
+}
+
+// Constant-matrix (mass) sweep without an intermediate array (exact banded LU,
+// precomputed factors):
+//   pass 1 eliminates forward through the whole fiber, keeping only the
+//          recurrence state (the last P values of y) at every chunk start
+//          (shared-memory checkpoints); the last chunk's y stays in registers;
+//   pass 2 walks the chunks backwards: re-reads the chunk's right-hand side
+//          (an L2 hit when the in-flight fibers fit -- grid sized for that),
+//          recomputes its forward elimination from the checkpoint and
+//          back-substitutes.
+// HBM traffic: read f (+ re-read misses), write x.  Chunk c+1 (pass 1) / c-1
+// (pass 2) is loaded while chunk c is being eliminated.
+template <int P, int CH>
+__global__ void __launch_bounds__(32 * SWEEP_WARPS)
+sweep_mass2_kernel(const SweepArgs A, int nck) {
+  constexpr int W = 2 * P + 1;
+  extern __shared__ double smem[];
+  const int wib = threadIdx.x >> 5;
+  double* fac = smem;                                                      // N * W
+  double* ck = smem + A.N * W + (size_t)wib * nck * P * 32;               // [nck][P][32] per warp
+  double(*T)[33] = reinterpret_cast<double(*)[33]>(smem + A.N * W + (size_t)SWEEP_WARPS * nck * P * 32) + wib * 32;
+  for (int x = threadIdx.x; x < A.N * W; x += blockDim.x) fac[x] = A.fac[x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * SWEEP_WARPS + wib;
+  const int nwarps = gridDim.x * SWEEP_WARPS;
+  const int lo = A.lo, hi = A.hi;
+  const int nc = (hi - lo + CH - 1) / CH;
+  if (nc <= 0) return;
+  for (int tile = warp; tile < A.ntiles; tile += nwarps) {
+    int64_t base, stride;
+    bool valid;
+    fiber_geom(A, tile, lane, base, stride, valid);
+    double v[CH], raw[CH];
+    double yw[P];
+#pragma unroll
+    for (int q = 0; q < P; q++) yw[q] = 0.0;
+    // ---- pass 1: forward elimination, checkpoints ----
+    issue_rows<CH>(A, A.in, tile, lane, base, stride, valid, lo, raw);
+    finish_rows<CH>(A, lane, T, raw, v);
+    for (int c = 0; c < nc; c++) {
+      const int c0 = lo + c * CH;
+      if (c + 1 < nc) issue_rows<CH>(A, A.in, tile, lane, base, stride, valid, c0 + CH, raw);
+#pragma unroll
+      for (int q = 0; q < P; q++) ck[(c * P + q) * 32 + lane] = yw[q];
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        const int row = c0 + r;
+        if (row < hi) {
+          const double* fr = fac + (row - lo) * W;
+          double y = v[r];
+#pragma unroll
+          for (int q = 0; q < P; q++) y = fma(-fr[q], yw[q], y);
+#pragma unroll
+          for (int q = P - 1; q > 0; q--) yw[q] = yw[q - 1];
+          yw[0] = y;
+          v[r] = y;
+        }
+      }
+      if (c + 1 < nc) finish_rows<CH>(A, lane, T, raw, v);
+    }
+    // v holds y of the last chunk
+    // ---- pass 2: backward substitution, chunk by chunk ----
+    double xw[P];
+#pragma unroll
+    for (int q = 0; q < P; q++) xw[q] = 0.0;
+    for (int c = nc - 1; c >= 0; c--) {
+      const int c0 = lo + c * CH;
+      if (c > 0) issue_rows<CH>(A, A.in, tile, lane, base, stride, valid, c0 - CH, raw);
+      if (c < nc - 1) {  // v holds f of chunk c: recompute its forward elimination
+#pragma unroll
+        for (int q = 0; q < P; q++) yw[q] = ck[(c * P + q) * 32 + lane];
+#pragma unroll
+        for (int r = 0; r < CH; r++) {
+          const double* fr = fac + (c0 + r - lo) * W;  // c0 + r < hi for every non-last chunk
+          double y = v[r];
+#pragma unroll
+          for (int q = 0; q < P; q++) y = fma(-fr[q], yw[q], y);
+#pragma unroll
+          for (int q = P - 1; q > 0; q--) yw[q] = yw[q - 1];
+          yw[0] = y;
+          v[r] = y;
+        }
+      }
+#pragma unroll
+      for (int r = CH - 1; r >= 0; r--) {
+        const int row = c0 + r;
+        if (row < hi) {
+          const double* fr = fac + (row - lo) * W;
+          double x = v[r];
+#pragma unroll
+          for (int q = 0; q < P; q++) x = fma(-fr[P + 1 + q], xw[q], x);
+          x *= fr[P];
+#pragma unroll
+          for (int q = P - 1; q > 0; q--) xw[q] = xw[q - 1];
+          xw[0] = x;
+          v[r] = x;
+        }
+      }
+      store_rows<CH>(A, A.out, tile, lane, base, stride, valid, c0, T, v);
+      if (c > 0) finish_rows<CH>(A, lane, T, raw, v);
     }
   }
 }

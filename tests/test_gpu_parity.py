@@ -59,6 +59,13 @@ def test_sweeps(n, p, axis):
     rng = np.random.default_rng(axis)
     for comp in (0, 1, 2, 3):
         rhs = rng.uniform(-1, 1, N ** 3)
+        if comp < 3:  # a sweep's input is zero outside the PEC active set (D1)
+            u = rhs.reshape(N, N, N)  # [k, j, i]
+            for ax in range(3):
+                if ax != comp:
+                    sl = [slice(None)] * 3
+                    sl[2 - ax] = [0, N - 1]
+                    u[tuple(sl)] = 0.0
         for mod in (False, True):
             if comp == 3 and mod:
                 continue
