@@ -20,10 +20,12 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "lib", "libadimaxwell.so")
-SOURCES = [os.path.join(_HERE, "csrc", "adi_maxwell.cu"), os.path.join(_HERE, "csrc", "kernels.cuh"),
-           os.path.join(_ROOT, "include", "adi_maxwell.h")]
+CSRC = os.path.join(_HERE, "csrc")
+SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "kernels.cuh", "dispatch.h", "setup_kernels.cuh")] + [
+    os.path.join(_ROOT, "include", "adi_maxwell.h")]
+DEGREES = (1, 2, 3, 4, 5)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
 
 ADI_OK, ADI_ERR_ARG, ADI_ERR_STATE, ADI_ERR_SINGULAR, ADI_ERR_CUDA, ADI_ERR_NCCL, ADI_ERR_OOM = range(7)
 ADI_BC_PEC, ADI_BC_NATURAL = 0, 1
@@ -38,17 +40,36 @@ EXPORTS = [
 ]
 
 
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libadimaxwell.so in-tree for sm_100a (nvcc; no GPU needed)."""
+    """Compile libadimaxwell.so in-tree for sm_100a (nvcc; no GPU needed).
+
+    One object per B-spline degree (csrc/degree.cu with -DADI_P=p) plus the host
+    orchestration (csrc/adi_maxwell.cu), compiled in parallel, then linked."""
     os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
     newest = max(os.path.getmtime(s) for s in SOURCES)
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
-        tmp = LIB_PATH + ".tmp"
-        cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, SOURCES[0]]
+    if not (force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest):
+        return LIB_PATH
+    objdir = os.path.join(os.path.dirname(LIB_PATH), "obj")
+    os.makedirs(objdir, exist_ok=True)
+    jobs = [(os.path.join(objdir, "adi_maxwell.o"), [os.path.join(CSRC, "adi_maxwell.cu")])]
+    for p in DEGREES:
+        jobs.append((os.path.join(objdir, f"degree_p{p}.o"), [f"-DADI_P={p}", os.path.join(CSRC, "degree.cu")]))
+    procs = []
+    for obj, args in jobs:
+        cmd = ["nvcc", *NVCC_FLAGS, "-c", "-o", obj, *args]
         if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
-        os.replace(tmp, LIB_PATH)
+            print(" ".join(cmd), flush=True)
+        procs.append((cmd, subprocess.Popen(cmd)))
+    bad = [cmd for cmd, pr in procs if pr.wait() != 0]
+    if bad:
+        raise RuntimeError("nvcc failed: " + " | ".join(" ".join(c) for c in bad))
+    tmp = LIB_PATH + ".tmp"
+    cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *[o for o, _ in jobs]]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 

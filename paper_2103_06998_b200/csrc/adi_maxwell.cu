@@ -19,7 +19,8 @@
 #include <vector>
 
 #include "../../include/adi_maxwell.h"
-#include "kernels.cuh"
+#include "dispatch.h"
+#include "setup_kernels.cuh"
 
 namespace {
 
@@ -284,120 +285,16 @@ bool make_field_map(CUtensorMap* m, const double* ptr, int N, int p) {
   return r == CUDA_SUCCESS;
 }
 
-template <int PP, int KIND, int S, int D>
-void rhs_tma_launch_t(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps) {
-  const int N = P->N;
-  adi::RhsTmaArgs ta;
-  ta.base = args;
-  memcpy(ta.yint, args.zint, sizeof ta.yint);
-  dim3 block(adi::RT_TX, adi::RT_THREADS / adi::RT_TX);
-  dim3 grid((N + adi::RT_TX - 1) / adi::RT_TX, (N + adi::RT_TY - 1) / adi::RT_TY, (N + args.kchunk - 1) / args.kchunk);
-  constexpr size_t smem = adi::rhs_tma_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
-  adi::rhs_tma_kernel<PP, KIND, S, D><<<grid, block, smem, P->stream>>>(maps, ta);
-}
-
-template <int PP, int KIND>
-void rhs_tma_launch_sd(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps, int s, int d) {
-  if (s == 1) {
-    if (d == 0) rhs_tma_launch_t<PP, KIND, 1, 0>(P, args, maps);
-    else if (d == 1) rhs_tma_launch_t<PP, KIND, 1, 1>(P, args, maps);
-    else rhs_tma_launch_t<PP, KIND, 1, 2>(P, args, maps);
-  } else {
-    if (d == 0) rhs_tma_launch_t<PP, KIND, 2, 0>(P, args, maps);
-    else if (d == 1) rhs_tma_launch_t<PP, KIND, 2, 1>(P, args, maps);
-    else rhs_tma_launch_t<PP, KIND, 2, 2>(P, args, maps);
-  }
-}
-
-template <int PP>
-void rhs_tma_launch_p(adi_patch P, const adi::RhsArgs& args, const adi::RhsTmaMaps& maps, int kind, int s, int d) {
-  if (kind == 0) rhs_tma_launch_sd<PP, 0>(P, args, maps, s, d);
-  else rhs_tma_launch_sd<PP, 1>(P, args, maps, s, d);
-}
-
-template <int PP, int KIND, int S, int D>
-cudaError_t rhs_tma_attr_t() {
-  constexpr size_t smem = adi::rhs_tma_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
-  return cudaFuncSetAttribute(adi::rhs_tma_kernel<PP, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-template <int PP>
-cudaError_t rhs_tma_attrs_p() {
-  cudaError_t e = cudaSuccess;
-  auto acc = [&](cudaError_t x) { if (x != cudaSuccess) e = x; };
-  acc(rhs_tma_attr_t<PP, 0, 1, 0>()); acc(rhs_tma_attr_t<PP, 0, 1, 1>()); acc(rhs_tma_attr_t<PP, 0, 1, 2>());
-  acc(rhs_tma_attr_t<PP, 0, 2, 0>()); acc(rhs_tma_attr_t<PP, 0, 2, 1>()); acc(rhs_tma_attr_t<PP, 0, 2, 2>());
-  acc(rhs_tma_attr_t<PP, 1, 1, 0>()); acc(rhs_tma_attr_t<PP, 1, 1, 1>()); acc(rhs_tma_attr_t<PP, 1, 1, 2>());
-  acc(rhs_tma_attr_t<PP, 1, 2, 0>()); acc(rhs_tma_attr_t<PP, 1, 2, 1>()); acc(rhs_tma_attr_t<PP, 1, 2, 2>());
-  return e;
-}
-
-cudaError_t rhs_tma_attrs(int p) {
+// degree dispatch (each degree's kernels live in their own translation unit)
+template <class F>
+auto with_degree(int p, F&& f) {
   switch (p) {
-    case 1: return rhs_tma_attrs_p<1>();
-    case 2: return rhs_tma_attrs_p<2>();
-    case 3: return rhs_tma_attrs_p<3>();
-    case 4: return rhs_tma_attrs_p<4>();
-    case 5: return rhs_tma_attrs_p<5>();
+    case 1: return f(adi::Ops<1>{});
+    case 2: return f(adi::Ops<2>{});
+    case 3: return f(adi::Ops<3>{});
+    case 4: return f(adi::Ops<4>{});
+    default: return f(adi::Ops<5>{});
   }
-  return cudaErrorInvalidValue;
-}
-
-template <int PP, int KIND, int S, int D>
-void rhs_launch_t(adi_patch P, const adi::RhsArgs& args) {
-  const int N = P->N;
-  dim3 block(adi::RHS_TX, adi::RHS_TY);
-  dim3 grid((N + adi::RHS_TX - 1) / adi::RHS_TX, (N + adi::RHS_TY - 1) / adi::RHS_TY,
-            (N + args.kchunk - 1) / args.kchunk);
-  constexpr size_t smem = adi::rhs_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
-  adi::rhs_kernel<PP, KIND, S, D><<<grid, block, smem, P->stream>>>(args);
-}
-
-template <int PP, int KIND, int S, int D>
-cudaError_t rhs_attr_t() {
-  constexpr size_t smem = adi::rhs_smem_bytes<PP, adi::RhsProg<KIND, S, D>::NT>();
-  return cudaFuncSetAttribute(adi::rhs_kernel<PP, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-template <int PP>
-cudaError_t rhs_attrs_p() {
-  cudaError_t e = cudaSuccess;
-  auto acc = [&](cudaError_t x) { if (x != cudaSuccess) e = x; };
-  acc(rhs_attr_t<PP, 0, 1, 0>()); acc(rhs_attr_t<PP, 0, 1, 1>()); acc(rhs_attr_t<PP, 0, 1, 2>());
-  acc(rhs_attr_t<PP, 0, 2, 0>()); acc(rhs_attr_t<PP, 0, 2, 1>()); acc(rhs_attr_t<PP, 0, 2, 2>());
-  acc(rhs_attr_t<PP, 1, 1, 0>()); acc(rhs_attr_t<PP, 1, 1, 1>()); acc(rhs_attr_t<PP, 1, 1, 2>());
-  acc(rhs_attr_t<PP, 1, 2, 0>()); acc(rhs_attr_t<PP, 1, 2, 1>()); acc(rhs_attr_t<PP, 1, 2, 2>());
-  return e;
-}
-
-cudaError_t rhs_attrs(int p) {
-  switch (p) {
-    case 1: return rhs_attrs_p<1>();
-    case 2: return rhs_attrs_p<2>();
-    case 3: return rhs_attrs_p<3>();
-    case 4: return rhs_attrs_p<4>();
-    case 5: return rhs_attrs_p<5>();
-  }
-  return cudaErrorInvalidValue;
-}
-
-template <int PP, int KIND>
-void rhs_launch_sd(adi_patch P, const adi::RhsArgs& args, int s, int d) {
-  if (s == 1) {
-    if (d == 0) rhs_launch_t<PP, KIND, 1, 0>(P, args);
-    else if (d == 1) rhs_launch_t<PP, KIND, 1, 1>(P, args);
-    else rhs_launch_t<PP, KIND, 1, 2>(P, args);
-  } else {
-    if (d == 0) rhs_launch_t<PP, KIND, 2, 0>(P, args);
-    else if (d == 1) rhs_launch_t<PP, KIND, 2, 1>(P, args);
-    else rhs_launch_t<PP, KIND, 2, 2>(P, args);
-  }
-}
-
-template <int PP>
-void rhs_launch_p(adi_patch P, const adi::RhsArgs& args, int kind, int s, int d) {
-  if (kind == 0) rhs_launch_sd<PP, 0>(P, args, s, d);
-  else rhs_launch_sd<PP, 1>(P, args, s, d);
 }
 
 // z-chunk length: enough blocks to fill the machine (>= ~4 waves), halo <= 25%
@@ -427,31 +324,21 @@ adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp
   }
   LaunchScope ls(P, cls);
   const int d = comp % 3;
+  const int N = P->N;
   if (P->use_tma) {
     adi::RhsTmaMaps maps;
     const int nt = kind == 0 ? 4 : 3;
     bool ok = true;
     for (int t = 0; t < nt; t++) ok = ok && make_field_map(&maps.m[t], args.u[t], P->N, P->p);
     if (ok) {
-      switch (P->p) {
-        case 1: rhs_tma_launch_p<1>(P, args, maps, kind, s, d); break;
-        case 2: rhs_tma_launch_p<2>(P, args, maps, kind, s, d); break;
-        case 3: rhs_tma_launch_p<3>(P, args, maps, kind, s, d); break;
-        case 4: rhs_tma_launch_p<4>(P, args, maps, kind, s, d); break;
-        case 5: rhs_tma_launch_p<5>(P, args, maps, kind, s, d); break;
-      }
+      dim3 grid((N + adi::RT_TX - 1) / adi::RT_TX, (N + adi::RT_TY - 1) / adi::RT_TY, (N + args.kchunk - 1) / args.kchunk);
+      with_degree(P->p, [&](auto ops) { ops.rhs_tma(P->stream, grid, args, maps, kind, s, d); });
       CUDA_TRY(cudaGetLastError());
       return ADI_OK;
     }
   }
-  switch (P->p) {
-    case 1: rhs_launch_p<1>(P, args, kind, s, d); break;
-    case 2: rhs_launch_p<2>(P, args, kind, s, d); break;
-    case 3: rhs_launch_p<3>(P, args, kind, s, d); break;
-    case 4: rhs_launch_p<4>(P, args, kind, s, d); break;
-    case 5: rhs_launch_p<5>(P, args, kind, s, d); break;
-    default: return fail(ADI_ERR_ARG, "rhs: bad p");
-  }
+  dim3 grid((N + adi::RHS_TX - 1) / adi::RHS_TX, (N + adi::RHS_TY - 1) / adi::RHS_TY, (N + args.kchunk - 1) / args.kchunk);
+  with_degree(P->p, [&](auto ops) { ops.rhs(P->stream, grid, args, kind, s, d); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
@@ -493,57 +380,35 @@ int64_t ntiles_axis(int N, int axis) {
   return (NN + 31) / 32;
 }
 
-template <int PP>
-adi_status launch_sweep_p(adi_patch P, const adi::SweepArgs& A, bool modified) {
-  const int W = 2 * PP + 1;
-  const int nsm = P->nsm;
-  size_t smem = (size_t)(modified ? 2 : 1) * P->N * W * sizeof(double);
-  if (A.axis == 0) smem += (size_t)adi::SWEEP_WARPS * 32 * 33 * sizeof(double);
+size_t sweep_smem(adi_patch P, int kind, int axis) {
+  const size_t W = P->W, N = P->N;
+  size_t words = (kind == adi::SW_MOD ? 2 : 1) * N * W;
+  if (kind == adi::SW_MASS) words += (size_t)adi::SWEEP_WARPS * ((N + 31) / 32) * P->p * 32;
+  if (axis == 0) words += (size_t)adi::SWEEP_WARPS * 32 * 33;
+  return words * sizeof(double);
+}
+
+adi_status launch_sweep(adi_patch P, const adi::SweepArgs& A, bool modified) {
+  const int kind = modified ? adi::SW_MOD : P->mass_v1 ? adi::SW_MASS_V1 : adi::SW_MASS;
   const int64_t blocks_needed = (A.ntiles + adi::SWEEP_WARPS - 1) / adi::SWEEP_WARPS;
-  const int64_t grid = std::min<int64_t>(blocks_needed, (int64_t)nsm * 16);
-  if (modified) {
-    constexpr int CH = 16;
-    auto k = adi::sweep_mod_kernel<PP, CH>;
-    k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
-  } else if (P->mass_v1) {
-    constexpr int CH = 32;
-    auto k = adi::sweep_mass_kernel<PP, CH>;
-    k<<<(unsigned)grid, 32 * adi::SWEEP_WARPS, smem, P->stream>>>(A);
-  } else {
-    constexpr int CH = 32;
-    const int nck = (P->N + CH - 1) / CH;
-    size_t smem2 = ((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * nck * PP * 32) * sizeof(double);
-    if (A.axis == 0) smem2 += (size_t)adi::SWEEP_WARPS * 32 * 33 * sizeof(double);
-    const int64_t grid2 = std::min<int64_t>(blocks_needed, (int64_t)nsm * P->mass_bps);
-    adi::sweep_mass2_kernel<PP, CH><<<(unsigned)grid2, 32 * adi::SWEEP_WARPS, smem2, P->stream>>>(A, nck);
-  }
+  const int64_t cap = kind == adi::SW_MASS ? (int64_t)P->nsm * P->mass_bps : (int64_t)P->nsm * 16;
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, cap);
+  const int nck = (P->N + 31) / 32;
+  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, sweep_smem(P, kind, A.axis), A, kind, nck); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
 
-template <int PP>
-adi_status sweep_attrs_p(adi_patch P) {
-  const int W = 2 * PP + 1;
-  const int mass = (int)(((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * 32 * 33) * sizeof(double));
-  const int mod = (int)(((size_t)2 * P->N * W + (size_t)adi::SWEEP_WARPS * 32 * 33) * sizeof(double));
-  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mass_kernel<PP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass));
-  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mod_kernel<PP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mod));
-  const int nck = (P->N + 31) / 32;
-  const int mass2 = (int)(((size_t)P->N * W + (size_t)adi::SWEEP_WARPS * nck * PP * 32 + (size_t)adi::SWEEP_WARPS * 32 * 33) *
-                          sizeof(double));
-  CUDA_TRY(cudaFuncSetAttribute(adi::sweep_mass2_kernel<PP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass2));
-  return ADI_OK;
-}
-
 adi_status sweep_attrs(adi_patch P) {
-  switch (P->p) {
-    case 1: return sweep_attrs_p<1>(P);
-    case 2: return sweep_attrs_p<2>(P);
-    case 3: return sweep_attrs_p<3>(P);
-    case 4: return sweep_attrs_p<4>(P);
-    case 5: return sweep_attrs_p<5>(P);
+  cudaError_t e = with_degree(P->p, [&](auto ops) {
+    return ops.sweep_attrs((int)sweep_smem(P, adi::SW_MASS_V1, 0), (int)sweep_smem(P, adi::SW_MASS, 0),
+                           (int)sweep_smem(P, adi::SW_MOD, 0));
+  });
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ADI_ERR_ARG, "N = %d too large for the sweep kernels' shared memory", P->N);
   }
-  return fail(ADI_ERR_ARG, "bad p");
+  return ADI_OK;
 }
 
 // One sweep along `axis` for component comp (active set per D1), in place on u
@@ -564,14 +429,7 @@ adi_status sweep(adi_patch P, int comp, int axis, bool modified, const double* i
   A.Sb = P->d_Sb[var];
   A.c = P->c;
   LaunchScope ls(P, modified ? ADI_K_SWEEP_MOD : ADI_K_SWEEP_MASS);
-  switch (P->p) {
-    case 1: return launch_sweep_p<1>(P, A, modified);
-    case 2: return launch_sweep_p<2>(P, A, modified);
-    case 3: return launch_sweep_p<3>(P, A, modified);
-    case 4: return launch_sweep_p<4>(P, A, modified);
-    case 5: return launch_sweep_p<5>(P, A, modified);
-  }
-  return fail(ADI_ERR_ARG, "sweep: bad p");
+  return launch_sweep(P, A, modified);
 }
 
 // E solve of component d, substep s: stiffened axis first (row-modified),
@@ -735,13 +593,7 @@ adi_status pivot_scan(adi_patch P) {
       unsigned long long init = ~0ull;
       CUDA_TRY(cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream));
       const unsigned grid = (unsigned)std::min<int64_t>((A.ntiles + 7) / 8, 148 * 8);
-      switch (P->p) {
-        case 1: adi::pivot_scan_kernel<1><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
-        case 2: adi::pivot_scan_kernel<2><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
-        case 3: adi::pivot_scan_kernel<3><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
-        case 4: adi::pivot_scan_kernel<4><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
-        case 5: adi::pivot_scan_kernel<5><<<grid, 256, 0, P->stream>>>(A, bad, 1e-14); break;
-      }
+      with_degree(P->p, [&](auto ops) { ops.pivot_scan(P->stream, grid, A, bad, 1e-14); });
       CUDA_TRY(cudaGetLastError());
       unsigned long long h = 0;
       CUDA_TRY(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, P->stream));
@@ -823,13 +675,13 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   if (const char* s = getenv("ADI_MASS_V1")) P->mass_v1 = atoi(s);
   if (const char* s = getenv("ADI_MASS_BPS")) P->mass_bps = std::max(1, atoi(s));
-  if (sweep_attrs(P)) return bail(fail(ADI_ERR_ARG, "N = %d too large for the sweep kernels' shared memory", N));
-  if (rhs_attrs(p) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
+  if (adi_status st0 = sweep_attrs(P)) return bail(st0);
+  if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   {
     const char* s = getenv("ADI_RHS_CPA");
     // TMA boxes no larger than the tensor (small patches use the cp.async kernel)
     P->use_tma = (N % 2 == 0) && N >= adi::RT_TX + 2 * p && tma_encoder() != nullptr && !(s && atoi(s));
-    if (P->use_tma && rhs_tma_attrs(p) != cudaSuccess) {
+    if (P->use_tma && with_degree(p, [](auto ops) { return ops.rhs_tma_attrs(); }) != cudaSuccess) {
       cudaGetLastError();
       P->use_tma = 0;
     }

@@ -1,0 +1,71 @@
+// setup_kernels.cuh -- amortised setup kernels (a0) of libadimaxwell.so:
+// material map (D6), row factors a, b, c, input validation, PEC
+// zeroing (D1).  Included by the host translation unit only.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace adi {
+
+// ---------------------------------------------------------------------------
+// Setup kernels (a0, amortised)
+// ---------------------------------------------------------------------------
+
+// One separable pass of the material map (D6): out[.., r, ..] = sum_e w[r*n + e] in[.., e, ..]
+// along `axis` of an (nx, ny, nz) array; output extent along the axis is N.
+__global__ void material_pass_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ w,
+                                     int n, int N, int p, int axis, int nx, int ny, int nz) {
+  // output dims
+  int ox = axis == 0 ? N : nx, oy = axis == 1 ? N : ny, oz = axis == 2 ? N : nz;
+  int64_t total = (int64_t)ox * oy * oz;
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    int x = (int)(id % ox);
+    int y = (int)((id / ox) % oy);
+    int z = (int)(id / ((int64_t)ox * oy));
+    int r = axis == 0 ? x : axis == 1 ? y : z;
+    double s = 0.0;
+    int e0 = r - p < 0 ? 0 : r - p;
+    int e1 = r < n - 1 ? r : n - 1;
+    for (int e = e0; e <= e1; e++) {
+      int xi = axis == 0 ? e : x, yi = axis == 1 ? e : y, zi = axis == 2 ? e : z;
+      s += w[r * n + e] * in[xi + (int64_t)nx * (yi + (int64_t)ny * zi)];
+    }
+    out[id] = s;
+  }
+}
+
+// a = tau/(2 eps), b = tau/(2 mu), c = tau^2/(4 eps mu)  (D13)
+__global__ void abc_kernel(const double* __restrict__ eps, const double* __restrict__ mu, double tau, int64_t U,
+                           double* __restrict__ a, double* __restrict__ b, double* __restrict__ c) {
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < U; I += (int64_t)gridDim.x * blockDim.x) {
+    const double e = eps[I], m = mu ? mu[I] : 1.0;
+    a[I] = tau / (2.0 * e);
+    b[I] = tau / (2.0 * m);
+    c[I] = tau * tau / (4.0 * e * m);
+  }
+}
+
+// validity check of positive finite values; writes the first offending index
+__global__ void check_positive_kernel(const double* __restrict__ x, int64_t n, unsigned long long* bad) {
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[I];
+    if (!(v > 0.0) || !isfinite(v)) atomicMin(bad, (unsigned long long)I);
+  }
+}
+
+// zero the PEC-eliminated entries of an E component (D1)
+__global__ void pec_zero_kernel(double* __restrict__ u, int N, int lo0, int hi0, int lo1, int hi1, int lo2, int hi2) {
+  const int64_t U = (int64_t)N * N * N;
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < U; I += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(I % N), j = (int)((I / N) % N), k = (int)(I / ((int64_t)N * N));
+    if (i < lo0 || i >= hi0 || j < lo1 || j >= hi1 || k < lo2 || k >= hi2) u[I] = 0.0;
+  }
+}
+
+__global__ void increment_kernel(int64_t* counter) { *counter += 1; }
+
+__global__ void fill_kernel(double* __restrict__ x, int64_t n, double v) {
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) x[I] = v;
+}
+
+}  // namespace adi
