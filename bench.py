@@ -57,7 +57,9 @@ def algorithmic_bytes(n: int, p: int):
       rhs_h      : 13 U * 8 B per substep (read H,E^old,E^new,b; write G), 3 launches
       sweep_mass : 16 B per active row (read rhs, write solution)
       sweep_mod  : 24 B per active row (read rhs and c, write solution)
-    Per step: 12 mass sweeps on E sets + 18 on H sets; 6 row-modified sweeps on E sets.
+    A sweep launch batches the three components (three jobs).  Per step: 4 mass
+    launches on E sets (3 x Ue rows each) + 6 on H sets (3 x U rows each); 2
+    row-modified launches on E sets (3 x Ue rows each).
     """
     N = n + p
     U = N ** 3
@@ -65,8 +67,8 @@ def algorithmic_bytes(n: int, p: int):
     return {
         "rhs_e": 11 * U * 8 / 3.0,
         "rhs_h": 13 * U * 8 / 3.0,
-        "sweep_mass": 16.0 * (12 * Ue + 18 * U) / 30.0,
-        "sweep_mod": 24.0 * Ue,
+        "sweep_mass": 16.0 * (12 * Ue + 18 * U) / 10.0,
+        "sweep_mod": 24.0 * 3 * Ue,
     }
 
 

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_PATH = os.path.join(_HERE, "lib", "libadimaxwell.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "kernels.cuh", "dispatch.h", "setup_kernels.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh")] + [
     os.path.join(_ROOT, "include", "adi_maxwell.h")]
 DEGREES = (1, 2, 3, 4, 5)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

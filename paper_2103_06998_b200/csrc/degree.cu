@@ -10,68 +10,39 @@ namespace adi {
 
 namespace {
 template <int KIND, int S, int D>
-void rhs_one(cudaStream_t st, dim3 grid, const RhsArgs& args) {
-  constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-  rhs_kernel<ADI_P, KIND, S, D><<<grid, dim3(RHS_TX, RHS_TY), smem, st>>>(args);
-}
-template <int KIND, int S, int D>
-void rhs_tma_one(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsTmaMaps& maps) {
-  RhsTmaArgs ta;
-  ta.base = args;
-  for (int o = 0; o < 3; o++)
-    for (int q = 0; q < 11; q++) ta.yint[o][q] = args.zint[o][q];
-  constexpr size_t smem = rhs_tma_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-  rhs_tma_kernel<ADI_P, KIND, S, D><<<grid, dim3(RT_TX, RT_THREADS / RT_TX), smem, st>>>(maps, ta);
-}
+struct RhsF {
+  static void run(cudaStream_t st, dim3 g, const RhsArgs& a, const RhsMaps& m, bool tma) {
+    constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
+    if (tma) rhs_kernel<ADI_P, KIND, S, D, true><<<g, RX_THREADS, smem, st>>>(m, a);
+    else rhs_kernel<ADI_P, KIND, S, D, false><<<g, RX_THREADS, smem, st>>>(m, a);
+  }
+};
 template <int KIND, int S, int D>
 cudaError_t rhs_attr_one() {
   constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
-template <int KIND, int S, int D>
-cudaError_t rhs_tma_attr_one() {
-  constexpr size_t smem = rhs_tma_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-  return cudaFuncSetAttribute(rhs_tma_kernel<ADI_P, KIND, S, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-// (kind, s, d) -> template arguments
-template <template <int, int, int> class F, class... Args>
-auto by_ksd(int kind, int s, int d, Args&&... a) {
-  const int code = kind * 6 + (s - 1) * 3 + d;
-  switch (code) {
-    case 0: return F<0, 1, 0>::run(a...);
-    case 1: return F<0, 1, 1>::run(a...);
-    case 2: return F<0, 1, 2>::run(a...);
-    case 3: return F<0, 2, 0>::run(a...);
-    case 4: return F<0, 2, 1>::run(a...);
-    case 5: return F<0, 2, 2>::run(a...);
-    case 6: return F<1, 1, 0>::run(a...);
-    case 7: return F<1, 1, 1>::run(a...);
-    case 8: return F<1, 1, 2>::run(a...);
-    case 9: return F<1, 2, 0>::run(a...);
-    case 10: return F<1, 2, 1>::run(a...);
-    default: return F<1, 2, 2>::run(a...);
-  }
-}
-template <int K, int S, int D>
-struct RhsF {
-  static void run(cudaStream_t st, dim3 g, const RhsArgs& a) { rhs_one<K, S, D>(st, g, a); }
-};
-template <int K, int S, int D>
-struct RhsTmaF {
-  static void run(cudaStream_t st, dim3 g, const RhsArgs& a, const RhsTmaMaps& m) { rhs_tma_one<K, S, D>(st, g, a, m); }
-};
 }  // namespace
 
 template <>
-void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, int kind, int s, int d) {
-  by_ksd<RhsF>(kind, s, d, st, grid, args);
-}
-
-template <>
-void Ops<ADI_P>::rhs_tma(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsTmaMaps& maps, int kind, int s,
-                         int d) {
-  by_ksd<RhsTmaF>(kind, s, d, st, grid, args, maps);
+void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind, int s,
+                     int d) {
+  switch (kind * 6 + (s - 1) * 3 + d) {
+    case 0: RhsF<0, 1, 0>::run(st, grid, args, maps, tma); break;
+    case 1: RhsF<0, 1, 1>::run(st, grid, args, maps, tma); break;
+    case 2: RhsF<0, 1, 2>::run(st, grid, args, maps, tma); break;
+    case 3: RhsF<0, 2, 0>::run(st, grid, args, maps, tma); break;
+    case 4: RhsF<0, 2, 1>::run(st, grid, args, maps, tma); break;
+    case 5: RhsF<0, 2, 2>::run(st, grid, args, maps, tma); break;
+    case 6: RhsF<1, 1, 0>::run(st, grid, args, maps, tma); break;
+    case 7: RhsF<1, 1, 1>::run(st, grid, args, maps, tma); break;
+    case 8: RhsF<1, 1, 2>::run(st, grid, args, maps, tma); break;
+    case 9: RhsF<1, 2, 0>::run(st, grid, args, maps, tma); break;
+    case 10: RhsF<1, 2, 1>::run(st, grid, args, maps, tma); break;
+    default: RhsF<1, 2, 2>::run(st, grid, args, maps, tma); break;
+  }
 }
 
 template <>
@@ -85,38 +56,40 @@ cudaError_t Ops<ADI_P>::rhs_attrs() {
   return e;
 }
 
+// sweep tiling: chunk of CH rows, ring of RS chunks per warp
+constexpr int SW_CH = 16;
+constexpr int SW_RS_MASS = 4;
+constexpr int SW_RS_MOD = 3;
+
 template <>
-cudaError_t Ops<ADI_P>::rhs_tma_attrs() {
-  cudaError_t e = cudaSuccess;
-  auto acc = [&](cudaError_t x) { if (x != cudaSuccess) e = x; };
-  acc(rhs_tma_attr_one<0, 1, 0>()); acc(rhs_tma_attr_one<0, 1, 1>()); acc(rhs_tma_attr_one<0, 1, 2>());
-  acc(rhs_tma_attr_one<0, 2, 0>()); acc(rhs_tma_attr_one<0, 2, 1>()); acc(rhs_tma_attr_one<0, 2, 2>());
-  acc(rhs_tma_attr_one<1, 1, 0>()); acc(rhs_tma_attr_one<1, 1, 1>()); acc(rhs_tma_attr_one<1, 1, 2>());
-  acc(rhs_tma_attr_one<1, 2, 0>()); acc(rhs_tma_attr_one<1, 2, 1>()); acc(rhs_tma_attr_one<1, 2, 2>());
-  return e;
+void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, bool modified) {
+  const unsigned block = 32 * SW_WARPS;
+  if (modified) {
+    constexpr size_t smem = sw_smem_bytes<ADI_P, true, SW_CH, SW_RS_MOD>();
+    sweep_kernel<ADI_P, true, SW_CH, SW_RS_MOD><<<grid, block, smem, st>>>(B);
+  } else {
+    constexpr size_t smem = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
+    sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS><<<grid, block, smem, st>>>(B);
+  }
 }
 
 template <>
-void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, size_t smem, const SweepArgs& A, int kind, int nck) {
-  const unsigned block = 32 * SWEEP_WARPS;
-  if (kind == SW_MOD) sweep_mod_kernel<ADI_P, 16><<<grid, block, smem, st>>>(A);
-  else if (kind == SW_MASS_V1) sweep_mass_kernel<ADI_P, 32><<<grid, block, smem, st>>>(A);
-  else sweep_mass2_kernel<ADI_P, 32><<<grid, block, smem, st>>>(A, nck);
-}
-
-template <>
-cudaError_t Ops<ADI_P>::sweep_attrs(int mass_smem, int mass2_smem, int mod_smem) {
+cudaError_t Ops<ADI_P>::sweep_attrs(int occ[2]) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(sweep_mass_kernel<ADI_P, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass_smem)))
-    return e;
-  if ((e = cudaFuncSetAttribute(sweep_mod_kernel<ADI_P, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mod_smem)))
-    return e;
-  return cudaFuncSetAttribute(sweep_mass2_kernel<ADI_P, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, mass2_smem);
+  constexpr size_t s0 = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
+  constexpr size_t s1 = sw_smem_bytes<ADI_P, true, SW_CH, SW_RS_MOD>();
+  auto k0 = sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS>;
+  auto k1 = sweep_kernel<ADI_P, true, SW_CH, SW_RS_MOD>;
+  if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0))) return e;
+  if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k0, 32 * SW_WARPS, s0))) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k1, 32 * SW_WARPS, s1);
 }
 
 template <>
-void Ops<ADI_P>::pivot_scan(cudaStream_t st, unsigned grid, const SweepArgs& A, unsigned long long* bad, double tol) {
-  pivot_scan_kernel<ADI_P><<<grid, 256, 0, st>>>(A, bad, tol);
+void Ops<ADI_P>::factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad,
+                        double tol) {
+  factor_kernel<ADI_P><<<grid, 128, 0, st>>>(B, iu, bad, tol);
 }
 
 }  // namespace adi

@@ -7,23 +7,24 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#include "kernels.cuh"
+#include "rhs.cuh"
+#include "sweep.cuh"
 
 namespace adi {
-
-enum SweepKind { SW_MASS_V1 = 0, SW_MASS = 1, SW_MOD = 2 };
 
 template <int P>
 struct Ops {
   // RHS of the E (kind 0) / H (kind 1) system of component d in substep s.
-  static void rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, int kind, int s, int d);
-  static void rhs_tma(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsTmaMaps& maps, int kind, int s, int d);
+  // tma: halo planes by cp.async.bulk.tensor (maps valid), else cp.async.
+  static void rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind, int s, int d);
   static cudaError_t rhs_attrs();
-  static cudaError_t rhs_tma_attrs();
-  // One sweep launch (grid, dynamic smem computed by the caller).
-  static void sweep(cudaStream_t st, unsigned grid, size_t smem, const SweepArgs& A, int kind, int nck);
-  static cudaError_t sweep_attrs(int mass_smem, int mass2_smem, int mod_smem);
-  static void pivot_scan(cudaStream_t st, unsigned grid, const SweepArgs& A, unsigned long long* bad, double tol);
+  // One batched sweep launch (persistent grid chosen by the caller).
+  static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, bool modified);
+  // Set the dynamic shared memory of both sweep kernels; occ[0|1] = resident
+  // blocks per SM of the mass / modified kernel.
+  static cudaError_t sweep_attrs(int occ[2]);
+  // Pivot cache of one row-modified family (job 0 of B).
+  static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };
 
 }  // namespace adi

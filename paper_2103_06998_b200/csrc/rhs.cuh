@@ -1,0 +1,355 @@
+// rhs.cuh -- right-hand sides of the E and H systems
+// as sums of row-scaled Kronecker products (X (x) Y (x) Z) u (P:233-258,
+// expanded per component in dupa1ab P:373-386), sum-factorised.
+//
+// One block owns a 32 x 16 (x, y) tile and streams a z-chunk of planes.  The
+// input planes of every term arrive with a P-wide x/y halo in a 3-deep
+// shared-memory ring (TMA cp.async.bulk.tensor + mbarrier when N is even so
+// that the 8-byte row pitch is 16-byte aligned; cp.async otherwise).  Per
+// plane: the x-pass (two outputs per thread, 128-bit shared loads) writes a
+// double-buffered x-filtered plane; the y-pass (two rows per thread) feeds a
+// (2P+1)-plane register window per term; the z-pass runs on that window.
+// Interior rows use the Toeplitz stencils from the parameter bank; the 2P
+// boundary rows at each end of an axis read the band tables.  Row scaling by
+// a, b, c and the PEC restriction (D1) are applied at the output.
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace adi {
+
+// 1D operator codes of the band tables: tab[(op*N + row)*(2P+1) + q] holds the
+// entry in column row-P+q (0 outside [0,N)).
+enum Op { OP_M = 0, OP_A = 1, OP_B = 2, OP_S = 3, NUM_OPS = 4 };
+enum Scale { SC_ONE = 0, SC_A = 1, SC_C = 2, SC_B = 3 };
+
+// The right-hand sides as compile-time "programs" of row-scaled Kronecker terms.
+// KIND 0 = E system of component D in substep S (a1/a5):
+//   R_D = M^3 E_D + a [ d_{D+1} H_{D+2} - d_{D+2} H_{D+1} ] + c (A on D, B on sigma) E_sigma,
+//   sigma = stiffened axis ((D+1)%3 in substep 1, (D+2)%3 in substep 2; K1/K2 of P:250-251);
+//   (discrete1/discrete3 P:235/241; expanded in dupa1ab P:373-386).
+// KIND 1 = H system of component D (a3/a7):
+//   S=1: G_D = M^3 H_D - b d_{D+1} Eo_{D+2} + b d_{D+2} En_{D+1}   (discrete2 P:238, C1/C2 P:254-255 + D3)
+//   S=2: G_D = M^3 H_D + b d_{D+2} Eo_{D+1} - b d_{D+1} En_{D+2}   (discrete4 P:244 with the sign D2)
+// "d_a" is the advection matrix A (derivative on the trial function, D4) on axis a.
+template <int KIND, int S, int D>
+struct RhsProg {
+  static constexpr int NT = KIND == 0 ? 4 : 3;
+  static constexpr int SIG = S == 1 ? (D + 1) % 3 : (D + 2) % 3;
+  __host__ __device__ static constexpr int op(int t, int ax) {
+    return t == 0 ? OP_M
+         : KIND == 0 ? (t == 1 ? (ax == (D + 1) % 3 ? OP_A : OP_M)
+                      : t == 2 ? (ax == (D + 2) % 3 ? OP_A : OP_M)
+                               : (ax == D ? OP_A : ax == SIG ? OP_B : OP_M))
+         : S == 1 ? (t == 1 ? (ax == (D + 1) % 3 ? OP_A : OP_M) : (ax == (D + 2) % 3 ? OP_A : OP_M))
+                  : (t == 1 ? (ax == (D + 2) % 3 ? OP_A : OP_M) : (ax == (D + 1) % 3 ? OP_A : OP_M));
+  }
+  __host__ __device__ static constexpr int scale(int t) {
+    return t == 0 ? SC_ONE : KIND == 0 ? (t == 3 ? SC_C : SC_A) : SC_B;
+  }
+  __host__ __device__ static constexpr double sign(int t) {
+    return t == 0 ? 1.0
+         : KIND == 0 ? (t == 2 ? -1.0 : 1.0)
+         : S == 1 ? (t == 1 ? -1.0 : 1.0) : (t == 1 ? 1.0 : -1.0);
+  }
+};
+
+constexpr int RX_TX = 32;
+constexpr int RX_TY = 16;
+constexpr int RX_THREADS = 256;  // 32 x 8, two output rows each
+constexpr int RX_MAXT = 4;
+constexpr int RX_RING = 3;
+
+struct RhsArgs {
+  int N;
+  int kchunk;                 // z-planes per block
+  const double* tab;          // band tables, 4 ops
+  const double* u[RX_MAXT];   // term inputs
+  const double* a;            // tau/(2 eps^)
+  const double* b;            // tau/(2 mu^)
+  const double* c;            // tau^2/(4 eps^ mu^)
+  const double* load;         // source load vector of this component, or nullptr (D9)
+  const double* signal;       // device signal array (nsig) or nullptr
+  const int64_t* step;        // device step counter
+  int64_t nsig;
+  int lo[3], hi[3];           // active ranges of the output component (PEC, D1)
+  double kint[3][11];         // interior (Toeplitz) rows of M, A, B (rows 2P..N-2P-1)
+  double* out;
+};
+
+struct RhsMaps {
+  CUtensorMap m[RX_MAXT];
+};
+
+template <int P>
+struct RxGeom {
+  static constexpr int W = 2 * P + 1;
+  static constexpr int HX = RX_TX + 2 * P;
+  static constexpr int HY = RX_TY + 2 * P;
+  static constexpr int PLANE = HX * HY;
+  static constexpr int PLANEP = (PLANE + 15) / 16 * 16;  // 128-byte aligned slices
+};
+
+template <int P, int NT>
+__host__ __device__ constexpr size_t rhs_smem_bytes() {
+  using G = RxGeom<P>;
+  return sizeof(double) * ((size_t)RX_RING * NT * G::PLANEP + (size_t)2 * NT * G::HY * RX_TX) +
+         RX_RING * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void rx_cp_async8(double* smem_dst, const double* gsrc, bool valid) {
+  const unsigned d = smem_u32(smem_dst);
+  const int sz = valid ? 8 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void rx_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void rx_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// out[I] = sum_t sign_t * scale_t[I] * ((X_t (x) Y_t (x) Z_t) u_t)[I]  (- a s J),
+// zero outside the active set.
+template <int P, int KIND, int S, int D, bool TMA>
+__global__ void __launch_bounds__(RX_THREADS, 2)
+rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs args) {
+  using Prog = RhsProg<KIND, S, D>;
+  using G = RxGeom<P>;
+  constexpr int NT = Prog::NT;
+  constexpr int W = G::W, HX = G::HX, HY = G::HY, PLANE = G::PLANE, PLANEP = G::PLANEP;
+  extern __shared__ __align__(1024) double rx_smem[];
+  double* ring = rx_smem;                                           // [RING][NT][PLANEP]
+  double* sx = rx_smem + RX_RING * NT * PLANEP;                     // [2][NT][HY][TX]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sx + 2 * NT * HY * RX_TX);  // [RING]
+
+  const int N = args.N;
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;  // y-pass / output: column tx, rows 2ty, 2ty+1
+  const int i0 = blockIdx.x * RX_TX, j0 = blockIdx.y * RX_TY;
+  const int k0 = blockIdx.z * args.kchunk;
+  const int k1 = min(N, k0 + args.kchunk);
+  const int i = i0 + tx;
+  const int jA = j0 + 2 * ty;
+  const int64_t NN = (int64_t)N * N;
+  const int kbeg = k0 - P, kend = k1 + P;  // input planes [kbeg, kend)
+
+  if (TMA) {
+    if (tid == 0) {
+      for (int s = 0; s < RX_RING; s++) mbar_init(&bar[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    }
+    __syncthreads();
+  }
+  // producer of input plane kin into its ring slot
+  auto produce = [&](int kin) {
+    const int st = (kin - kbeg) % RX_RING;
+    double* slot = ring + st * NT * PLANEP;
+    if (TMA) {
+      if (tid == 0) {
+        if (kin < kend) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_expect_tx(&bar[st], (unsigned)(NT * PLANE * sizeof(double)));
+#pragma unroll
+          for (int t = 0; t < NT; t++) tma_load_3d(slot + t * PLANEP, &maps.m[t], i0 - P, j0 - P, kin, &bar[st]);
+        }
+      }
+    } else {
+      if (kin < kend) {
+        const bool kok = kin >= 0 && kin < N;
+        const int64_t pb = kok ? NN * kin : 0;
+        for (int e = tid; e < PLANE; e += RX_THREADS) {
+          const int yy = e / HX, xx = e - yy * HX;
+          const int gi = i0 - P + xx, gj = j0 - P + yy;
+          const bool ok = kok && gi >= 0 && gi < N && gj >= 0 && gj < N;
+          const int64_t off = ok ? pb + gi + (int64_t)N * gj : 0;
+#pragma unroll
+          for (int t = 0; t < NT; t++) rx_cp_async8(slot + t * PLANEP + e, args.u[t] + off, ok);
+        }
+      }
+      rx_commit();  // (empty groups keep the wait arithmetic uniform)
+    }
+  };
+  produce(kbeg);
+  produce(kbeg + 1);
+  produce(kbeg + 2);
+
+  double w[NT][2][W];
+#pragma unroll
+  for (int t = 0; t < NT; t++)
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+      for (int q = 0; q < W; q++) w[t][r][q] = 0.0;
+  double sval = 0.0;
+  if (KIND == 0 && args.load != nullptr && args.signal != nullptr) {
+    const int64_t s = *args.step;
+    if (s < args.nsig) sval = args.signal[s];
+  }
+  const bool yin = jA >= 2 * P && jA + 1 < N - 2 * P;  // both output rows Toeplitz in y
+
+  for (int g0 = kbeg; g0 < kend; g0 += W) {
+#pragma unroll
+    for (int ph = 0; ph < W; ph++) {
+      const int kin = g0 + ph;
+      if (kin < kend) {
+        const int it = kin - kbeg;
+        const int st = it % RX_RING;
+        const double* slot = ring + st * NT * PLANEP;
+        double* sxb = sx + (it & 1) * NT * HY * RX_TX;
+        // prefetch the row scales of the output plane k = kin - P
+        const int k = kin - P;
+        const bool kout = k >= k0 && i < N;
+        double sc[2][3];
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+          const int j = jA + r;
+          const bool ok = kout && j < N;
+          const int64_t I = ok ? i + (int64_t)N * j + NN * k : 0;
+          if (KIND == 0) {
+            sc[r][0] = ok ? args.a[I] : 0.0;
+            sc[r][1] = ok ? args.c[I] : 0.0;
+            sc[r][2] = (ok && sval != 0.0) ? args.load[I] : 0.0;
+          } else {
+            sc[r][0] = ok ? args.b[I] : 0.0;
+            sc[r][1] = sc[r][2] = 0.0;
+          }
+        }
+        if (TMA) {
+          mbar_wait(&bar[st], (unsigned)((it / RX_RING) & 1));
+        } else {
+          rx_wait<RX_RING - 1>();
+          __syncthreads();
+        }
+        // ---- x-pass: rows yy of every term, two outputs (2u, 2u+1) per task
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int xop = Prog::op(t, 0);
+          for (int task = tid; task < HY * 16; task += RX_THREADS) {
+            const int yy = task >> 4, u = task & 15;
+            const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
+            double v[2 * P + 2];
+#pragma unroll
+            for (int q = 0; q <= P; q++) {
+              const double2 d2 = rp[q];
+              v[2 * q] = d2.x;
+              v[2 * q + 1] = d2.y;
+            }
+            const int x0 = i0 + 2 * u;
+            double o0 = 0.0, o1 = 0.0;
+            if (x0 >= 2 * P && x0 + 1 < N - 2 * P) {
+#pragma unroll
+              for (int q = 0; q < W; q++) {
+                o0 = fma(args.kint[xop][q], v[q], o0);
+                o1 = fma(args.kint[xop][q], v[q + 1], o1);
+              }
+            } else {
+              const double* c0 = args.tab + ((int64_t)xop * N + x0) * W;
+              const bool ok0 = x0 < N, ok1 = x0 + 1 < N;
+#pragma unroll
+              for (int q = 0; q < W; q++) {
+                o0 = fma(ok0 ? __ldg(c0 + q) : 0.0, v[q], o0);
+                o1 = fma(ok1 ? __ldg(c0 + W + q) : 0.0, v[q + 1], o1);
+              }
+            }
+            *reinterpret_cast<double2*>(sxb + (t * HY + yy) * RX_TX + 2 * u) = make_double2(o0, o1);
+          }
+        }
+        __syncthreads();  // x-pass(kin) visible; ring slot st free; y-pass(kin-1) used the other sx buffer
+        produce(kin + RX_RING);
+        // ---- y-pass: rows 2ty, 2ty+1 of column tx -> z-window slot ph
+#pragma unroll
+        for (int t = 0; t < NT; t++) {
+          const int yop = Prog::op(t, 1);
+          double col[W + 1];
+#pragma unroll
+          for (int q = 0; q <= W; q++) col[q] = sxb[(t * HY + 2 * ty + q) * RX_TX + tx];
+          double vA = 0.0, vB = 0.0;
+          if (yin) {
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+              vA = fma(args.kint[yop][q], col[q], vA);
+              vB = fma(args.kint[yop][q], col[q + 1], vB);
+            }
+          } else {
+            const double* cA = args.tab + ((int64_t)yop * N + jA) * W;
+            const bool okA = jA < N, okB = jA + 1 < N;
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+              vA = fma(okA ? __ldg(cA + q) : 0.0, col[q], vA);
+              vB = fma(okB ? __ldg(cA + W + q) : 0.0, col[q + 1], vB);
+            }
+          }
+          w[t][0][ph] = vA;
+          w[t][1][ph] = vB;
+        }
+        // ---- z-pass + row scaling for the output plane k = kin - P
+        if (kout) {
+          const bool zin = k >= 2 * P && k < N - 2 * P;
+          const bool ak = k >= args.lo[2] && k < args.hi[2] && i >= args.lo[0] && i < args.hi[0];
+#pragma unroll
+          for (int r = 0; r < 2; r++) {
+            const int j = jA + r;
+            if (j < N) {
+              double zs[3] = {0.0, 0.0, 0.0};  // scale groups: one, a|b, c
+#pragma unroll
+              for (int t = 0; t < NT; t++) {
+                const int zop = Prog::op(t, 2);
+                double z = 0.0;
+                if (zin) {
+#pragma unroll
+                  for (int q = 0; q < W; q++) z = fma(args.kint[zop][q], w[t][r][(ph + 1 + q) % W], z);
+                } else {
+                  const double* zc = args.tab + ((int64_t)zop * N + k) * W;
+#pragma unroll
+                  for (int q = 0; q < W; q++) z = fma(__ldg(zc + q), w[t][r][(ph + 1 + q) % W], z);
+                }
+                const int grp = Prog::scale(t) == SC_ONE ? 0 : Prog::scale(t) == SC_C ? 2 : 1;
+                zs[grp] = fma(Prog::sign(t), z, zs[grp]);
+              }
+              double val = 0.0;
+              if (ak && j >= args.lo[1] && j < args.hi[1]) {
+                if (KIND == 0) {
+                  val = zs[0] + sc[r][0] * zs[1] + sc[r][1] * zs[2];
+                  if (sval != 0.0) val -= sc[r][0] * sval * sc[r][2];
+                } else {
+                  val = zs[0] + sc[r][0] * zs[1];
+                }
+              }
+              args.out[i + (int64_t)N * j + NN * k] = val;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!TMA) rx_wait<0>();
+}
+
+}  // namespace adi

@@ -1,0 +1,455 @@
+// sweep.cuh -- batched banded sweeps along one axis for every fiber
+// (P:468-527 systems A, B, C; row-modified form P:529-594 / Appendix).
+//
+// One lane solves one fiber; a warp owns a tile of 32 fibers; a launch carries
+// up to three independent jobs (e.g. the three field components, each with its
+// own axis and PEC row range, D1).  Per tile:
+//   pass 1  streams the fiber rows forward through a per-warp cp.async ring in
+//           shared memory (RS chunks of CH rows in flight), runs the forward
+//           elimination and stores only the recurrence state at every chunk
+//           start (a per-warp checkpoint slot in global memory, L2-resident);
+//   pass 2  walks the chunks backwards: the ring re-loads a chunk (an L2 hit
+//           for recently streamed fibers), the forward elimination of that
+//           chunk is recomputed from its checkpoint and the back substitution
+//           writes the solution.
+// HBM traffic is the algorithmic minimum: read f (and c, pivots), write x.
+//
+// Constant (mass) matrix: precomputed LU factors; rows [hk, tk) equal the
+// interior factor row bit for bit and come from the kernel parameters.
+// Row-modified matrix M + diag(c) S (c = tau^2/(4 eps^ mu^) of the row's test
+// function): the pivots 1/u_kk are cached per fiber at set_materials/set_tau
+// (factor_kernel); the multipliers and the U row are recomputed from c in
+// registers, so the recurrence carries no division.  No pivoting (D12; the
+// factor kernel rejects tiny pivots).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace adi {
+
+constexpr int SW_MAXJOBS = 3;
+constexpr int SW_WARPS = 4;  // warps per block
+
+struct SweepJob {
+  const double* in;   // right-hand side (N^3)
+  double* out;        // solution (may equal in)
+  const double* c;    // per-test-function c (modified sweeps)
+  const double* iu;   // cached pivots 1/u_kk of this family (modified sweeps)
+  int axis;           // 0 = x, 1 = y, 2 = z
+  int lo, hi;         // active rows along the axis (PEC, D1)
+  int var;            // band-table variant: 0 = [0,N), 1 = [1,N-1)
+};
+
+struct SweepBatch {
+  SweepJob job[SW_MAXJOBS];
+  int njobs;
+  int N;
+  int ntiles;          // 32-fiber tiles per job = ceil(N^2 / 32)
+  int nck;             // checkpoint slots per warp (chunks per fiber)
+  double* ckpt;        // per-warp checkpoint slots
+  // constant (mass) factors per variant: rows = absolute row index, W entries:
+  //   [0..P-1] l_{k,k-1-q}, [P] 1/u_kk, [P+1..2P] u_{k,k+1+q}
+  const double* fac[2];
+  int hk[2], tk[2];    // rows in [hk, tk) equal kfac bit for bit
+  double kfac[2][11];
+  // row-modified: band rows of M and S restricted to the variant's range
+  const double* Mb[2];
+  const double* Sb[2];
+  double kM[11], kS[11];  // interior Toeplitz rows (rows in [2P, N-2P))
+};
+
+__device__ __forceinline__ void sw_cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void sw_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void sw_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int P, bool MOD, int CH>
+__host__ __device__ constexpr int sw_slot_doubles() {
+  return (MOD ? 3 : 1) * CH * 33;
+}
+template <int P, bool MOD, int CH, int RS>
+constexpr size_t sw_smem_bytes() {
+  return sizeof(double) * (size_t)SW_WARPS * RS * sw_slot_doubles<P, MOD, CH>();
+}
+template <int P, bool MOD>
+__host__ __device__ constexpr int sw_state_words() {
+  return MOD ? P * (P + 2) : P;
+}
+
+template <int P, bool MOD, int CH, int RS>
+__global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const __grid_constant__ SweepBatch B) {
+  constexpr int W = 2 * P + 1;
+  constexpr int NA = MOD ? 3 : 1;
+  constexpr int SLOT = sw_slot_doubles<P, MOD, CH>();
+  constexpr int SWD = sw_state_words<P, MOD>();
+  extern __shared__ double sw_smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* ring = sw_smem + (size_t)wib * RS * SLOT;
+  const int gw = blockIdx.x * SW_WARPS + wib;
+  const int nw = gridDim.x * SW_WARPS;
+  const int N = B.N;
+  const int64_t NN = (int64_t)N * N;
+  double* ck = B.ckpt + (size_t)gw * B.nck * SWD * 32 + lane;
+  const int total = B.njobs * B.ntiles;
+
+  for (int t = gw; t < total; t += nw) {
+    const int jb = t / B.ntiles;
+    const int tile = t - jb * B.ntiles;
+    const double* src[3];
+    double* out;
+    int axis, lo, hi, var;
+    {
+      const SweepJob& J = jb == 0 ? B.job[0] : jb == 1 ? B.job[1] : B.job[2];
+      src[0] = J.in;
+      src[1] = J.c;
+      src[2] = J.iu;
+      out = J.out;
+      axis = J.axis;
+      lo = J.lo;
+      hi = J.hi;
+      var = J.var;
+    }
+    const int64_t f0 = (int64_t)tile * 32;
+    const int64_t f = f0 + lane;
+    const bool fval = f < NN;
+    const int64_t fc = fval ? f : NN - 1;  // invalid lanes load (and never store) a valid fiber
+    int64_t base, stride;
+    if (axis == 2) {
+      base = fc;
+      stride = NN;
+    } else if (axis == 1) {
+      base = (fc % N) + NN * (fc / N);
+      stride = N;
+    } else {
+      base = (int64_t)N * fc;
+      stride = 1;
+    }
+    const int nc = (hi - lo + CH - 1) / CH;
+    // x axis: lane loads row (lane % CH) of fiber m*(32/CH) + lane/CH, m = 0..CH-1
+    constexpr int FPI = 32 / CH;
+    const int xr = lane % CH, xf = lane / CH;
+
+    // chunk c of the tile -> ring slot c % RS (layout [array][row][33], lane = fiber).
+    // Rows past hi are not loaded (the compute skips them).
+    auto issue = [&](int c) {
+      double* sl = ring + (c % RS) * SLOT;
+      const int r0 = lo + c * CH;
+      const int nr = min(CH, hi - r0);
+      if (axis != 0) {
+        const double* p0 = src[0] + base + (int64_t)r0 * stride;
+        const double* p1 = MOD ? src[1] + base + (int64_t)r0 * stride : nullptr;
+        const double* p2 = MOD ? src[2] + base + (int64_t)r0 * stride : nullptr;
+#pragma unroll
+        for (int r = 0; r < CH; r++) {
+          if (r < nr) {
+            sw_cp_async8(sl + r * 33 + lane, p0);
+            if (MOD) {
+              sw_cp_async8(sl + (CH + r) * 33 + lane, p1);
+              sw_cp_async8(sl + (2 * CH + r) * 33 + lane, p2);
+            }
+          }
+          p0 += stride;
+          if (MOD) p1 += stride, p2 += stride;
+        }
+      } else {
+        const int row = min(r0 + xr, hi - 1);
+        const int64_t o0 = (int64_t)N * f0 + row;
+        const int64_t fmax = NN - 1 - f0;  // last valid fiber offset in the tile
+#pragma unroll
+        for (int m = 0; m < CH; m++) {
+          const int ff = m * FPI + xf;
+          const int64_t off = ff <= fmax ? o0 + (int64_t)N * ff : o0;
+          double* d = sl + xr * 33 + ff;
+          sw_cp_async8(d, src[0] + off);
+          if (MOD) {
+            sw_cp_async8(d + CH * 33, src[1] + off);
+            sw_cp_async8(d + 2 * CH * 33, src[2] + off);
+          }
+        }
+      }
+      sw_commit();
+    };
+
+    // recurrence state: yw[m-1] = y_{k-m}; (MOD) uw[m-1][j-1] = u_{k-m,k-m+j}, iw[m-1] = 1/u_{k-m,k-m}
+    double yw[P];
+    double uw[MOD ? P : 1][P];
+    double iw[MOD ? P : 1];
+#pragma unroll
+    for (int m = 0; m < P; m++) yw[m] = 0.0;
+    if (MOD) {
+#pragma unroll
+      for (int m = 0; m < P; m++) {
+        iw[m] = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; j++) uw[m][j] = 0.0;
+      }
+    }
+
+    // row k of the modified matrix: a[q] = M_{k,k-P+q} + c_k S_{k,k-P+q}
+    auto mod_row = [&](int row, double cc, double* a) {
+      const bool in = row >= 2 * P && row < N - 2 * P;
+      const double* mr = B.Mb[var] + (size_t)row * W;
+      const double* sr = B.Sb[var] + (size_t)row * W;
+#pragma unroll
+      for (int q = 0; q < W; q++) {
+        const double mq = in ? B.kM[q] : __ldg(mr + q);
+        const double sq = in ? B.kS[q] : __ldg(sr + q);
+        a[q] = fma(cc, sq, mq);
+      }
+    };
+    // one forward elimination step (row k): returns y_k, and (MOD) u_{k,k+q}, q = 1..P in un[]
+    auto fwd = [&](int row, double fv, double cc, double ivk, double* un) -> double {
+      double y = fv;
+      if (MOD) {
+        double a[W];
+        mod_row(row, cc, a);
+        double l[P + 1];
+#pragma unroll
+        for (int m = P; m >= 1; m--) {
+          double s = a[P - m];
+#pragma unroll
+          for (int mp = P; mp > m; mp--) s = fma(-l[mp], uw[mp - 1][mp - m - 1], s);
+          l[m] = s * iw[m - 1];
+        }
+#pragma unroll
+        for (int q = 1; q <= P; q++) {
+          double s = a[P + q];
+#pragma unroll
+          for (int m = 1; m + q <= P; m++) s = fma(-l[m], uw[m - 1][m + q - 1], s);
+          un[q - 1] = s;
+        }
+#pragma unroll
+        for (int m = P; m >= 1; m--) y = fma(-l[m], yw[m - 1], y);
+#pragma unroll
+        for (int m = P - 1; m > 0; m--) {
+          iw[m] = iw[m - 1];
+#pragma unroll
+          for (int j = 0; j < P; j++) uw[m][j] = uw[m - 1][j];
+        }
+        iw[0] = ivk;
+#pragma unroll
+        for (int j = 0; j < P; j++) uw[0][j] = un[j];
+      } else {
+        const bool in = row >= B.hk[var] && row < B.tk[var];
+        const double* fr = B.fac[var] + (size_t)row * W;
+#pragma unroll
+        for (int q = P - 1; q >= 0; q--) y = fma(-(in ? B.kfac[var][q] : __ldg(fr + q)), yw[q], y);
+      }
+#pragma unroll
+      for (int m = P - 1; m > 0; m--) yw[m] = yw[m - 1];
+      yw[0] = y;
+      return y;
+    };
+    auto save_state = [&](int c) {
+      double* p = ck + (size_t)c * SWD * 32;
+#pragma unroll
+      for (int m = 0; m < P; m++) p[m * 32] = yw[m];
+      if (MOD) {
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+          p[(P + m) * 32] = iw[m];
+#pragma unroll
+          for (int j = 0; j < P; j++) p[(2 * P + m * P + j) * 32] = uw[m][j];
+        }
+      }
+    };
+    auto set_state = [&](const double* p) {
+#pragma unroll
+      for (int m = 0; m < P; m++) yw[m] = p[m];
+      if (MOD) {
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+          iw[m] = p[P + m];
+#pragma unroll
+          for (int j = 0; j < P; j++) uw[m][j] = p[2 * P + m * P + j];
+        }
+      }
+    };
+
+    // ---------------- pass 1: forward elimination, checkpoints ----------------
+#pragma unroll
+    for (int c = 0; c < RS - 1; c++) {
+      if (c < nc) issue(c);
+      else sw_commit();
+    }
+    for (int c = 0; c < nc; c++) {
+      sw_wait<RS - 2>();
+      __syncwarp();
+      save_state(c);
+      const double* sl = ring + (c % RS) * SLOT;
+      const int r0 = lo + c * CH;
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        const int row = r0 + r;
+        if (row < hi) {
+          double un[P];
+          fwd(row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0, MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0,
+              un);
+        }
+      }
+      __syncwarp();
+      if (c + RS - 1 < nc) issue(c + RS - 1);
+      else sw_commit();
+    }
+    // ---------------- pass 2: recompute per chunk, back substitution ----------
+    double xw[P];
+#pragma unroll
+    for (int q = 0; q < P; q++) xw[q] = 0.0;
+    double nxt[SWD];  // checkpoint of the next chunk to process, loaded one iteration ahead
+#pragma unroll
+    for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(nc - 1) * SWD + q) * 32];
+    for (int c = nc - 1; c >= 0; c--) {
+      if (c < nc - RS) {  // not resident from pass 1: issued RS-1 iterations ago
+        sw_wait<RS - 2>();
+      }
+      __syncwarp();
+      double* sl = ring + (c % RS) * SLOT;
+      const int r0 = lo + c * CH;
+      set_state(nxt);
+      if (c > 0) {
+#pragma unroll
+        for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(c - 1) * SWD + q) * 32];
+      }
+      double y[CH];
+      double us[CH][MOD && P > 1 ? P - 1 : 1];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        const int row = r0 + r;
+        y[r] = 0.0;
+        if (row < hi) {
+          double un[P];
+          y[r] = fwd(row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
+                     MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
+          if (MOD) {
+#pragma unroll
+            for (int q = 0; q < P - 1; q++) us[r][q] = un[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int r = CH - 1; r >= 0; r--) {
+        const int row = r0 + r;
+        if (row < hi) {
+          double x = y[r];
+          if (MOD) {
+            const double cc = sl[(CH + r) * 33 + lane];
+            double a[W];
+            mod_row(row, cc, a);
+            x = fma(-a[2 * P], xw[P - 1], x);
+#pragma unroll
+            for (int q = P - 1; q >= 1; q--) x = fma(-us[r][q - 1], xw[q - 1], x);
+            x *= sl[(2 * CH + r) * 33 + lane];
+          } else {
+            const bool in = row >= B.hk[var] && row < B.tk[var];
+            const double* fr = B.fac[var] + (size_t)row * W;
+#pragma unroll
+            for (int q = P - 1; q >= 0; q--) x = fma(-(in ? B.kfac[var][P + 1 + q] : __ldg(fr + P + 1 + q)), xw[q], x);
+            x *= in ? B.kfac[var][P] : __ldg(fr + P);
+          }
+#pragma unroll
+          for (int q = P - 1; q > 0; q--) xw[q] = xw[q - 1];
+          xw[0] = x;
+          y[r] = x;
+        }
+      }
+      // store the chunk
+      if (axis != 0) {
+        double* po = out + base + (int64_t)r0 * stride;
+#pragma unroll
+        for (int r = 0; r < CH; r++) {
+          if (fval && r0 + r < hi) *po = y[r];
+          po += stride;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
+        __syncwarp();
+        const int row = r0 + xr;
+        double* po = out + (int64_t)N * f0 + row;
+#pragma unroll
+        for (int m = 0; m < CH; m++) {
+          const int ff = m * FPI + xf;
+          if (f0 + ff < NN && row < hi) po[(int64_t)N * ff] = sl[xr * 33 + ff];
+        }
+      }
+      __syncwarp();
+      // ring slot (c+1)%RS is free (chunk c+1 done): fetch chunk c+1-RS into it
+      if (c < nc - 1 && c + 1 - RS >= 0) issue(c + 1 - RS);
+      else sw_commit();
+    }
+    sw_wait<0>();
+    __syncwarp();
+  }
+}
+
+// Pivot cache of one row-modified family (set_materials / set_tau, amortised):
+// for every fiber along `axis`, the no-pivot banded LU of M + diag(c) S on
+// [lo, hi) in the same arithmetic as sweep_kernel<MOD>; writes 1/u_kk and
+// records the first fiber with |u_kk| < tol * max|row| (D12 gate).
+template <int P>
+__global__ void factor_kernel(const SweepBatch B, double* __restrict__ iu_out, unsigned long long* bad, double tol) {
+  constexpr int W = 2 * P + 1;
+  const SweepJob& J = B.job[0];
+  const int N = B.N;
+  const int64_t NN = (int64_t)N * N;
+  const int var = J.var;
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < NN; f += (int64_t)gridDim.x * blockDim.x) {
+    int64_t base, stride;
+    if (J.axis == 2) {
+      base = f;
+      stride = NN;
+    } else if (J.axis == 1) {
+      base = (f % N) + NN * (f / N);
+      stride = N;
+    } else {
+      base = (int64_t)N * f;
+      stride = 1;
+    }
+    double uw[P][P], iw[P];
+    for (int m = 0; m < P; m++) {
+      iw[m] = 0.0;
+      for (int j = 0; j < P; j++) uw[m][j] = 0.0;
+    }
+    bool failed = false;
+    for (int row = J.lo; row < J.hi; row++) {
+      const double cc = J.c[base + (int64_t)row * stride];
+      const bool in = row >= 2 * P && row < N - 2 * P;
+      double a[W], amax = 0.0;
+      for (int q = 0; q < W; q++) {
+        const double mq = in ? B.kM[q] : B.Mb[var][(size_t)row * W + q];
+        const double sq = in ? B.kS[q] : B.Sb[var][(size_t)row * W + q];
+        a[q] = fma(cc, sq, mq);
+        amax = fmax(amax, fabs(a[q]));
+      }
+      double l[P + 1];
+      for (int m = P; m >= 1; m--) {
+        double s = a[P - m];
+        for (int mp = P; mp > m; mp--) s = fma(-l[mp], uw[mp - 1][mp - m - 1], s);
+        l[m] = s * iw[m - 1];
+      }
+      double u0 = a[P];
+      for (int m = 1; m <= P; m++) u0 = fma(-l[m], uw[m - 1][m - 1], u0);
+      double un[P];
+      for (int q = 1; q <= P; q++) {
+        double s = a[P + q];
+        for (int m = 1; m + q <= P; m++) s = fma(-l[m], uw[m - 1][m + q - 1], s);
+        un[q - 1] = s;
+      }
+      if (!(fabs(u0) >= tol * amax)) failed = true;
+      const double ivk = failed ? 0.0 : 1.0 / u0;
+      iu_out[base + (int64_t)row * stride] = ivk;
+      for (int m = P - 1; m > 0; m--) {
+        iw[m] = iw[m - 1];
+        for (int j = 0; j < P; j++) uw[m][j] = uw[m - 1][j];
+      }
+      iw[0] = ivk;
+      for (int j = 0; j < P; j++) uw[0][j] = un[j];
+    }
+    if (failed) atomicMin(bad, (unsigned long long)f);
+  }
+}
+
+}  // namespace adi
