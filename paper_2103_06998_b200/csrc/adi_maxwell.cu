@@ -383,7 +383,6 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
   B.N = P->N;
   B.njobs = nreq;
   B.ntiles = (int)(((int64_t)P->N * P->N + 31) / 32);
-  B.nck = (P->N + 15) / 16;
   B.ckpt = P->ckpt;
   for (int j = 0; j < nreq; j++) {
     adi::SweepJob& J = B.job[j];
@@ -409,6 +408,7 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
 
 adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, bool modified) {
   adi::SweepBatch B = make_batch(P, req, nreq);
+  B.nck = (P->N + (modified ? adi::SW_CH_MOD : adi::SW_CH_MASS) - 1) / (modified ? adi::SW_CH_MOD : adi::SW_CH_MASS);
   LaunchScope ls(P, modified ? ADI_K_SWEEP_MOD : ADI_K_SWEEP_MASS);
   const int64_t warps_needed = (int64_t)nreq * B.ntiles;
   const int64_t blocks_needed = (warps_needed + adi::SW_WARPS - 1) / adi::SW_WARPS;
@@ -711,6 +711,18 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   }
   Space1D sp(P->n, p);
   assemble_1d(sp, P->M, P->S, P->A);
+  // Uniform knots make rows [2p, N-2p) of M, S, A translates of one stencil
+  // (P:429-440); quadrature at shifted points leaves them equal only to
+  // ~1e-16 relative.  Copy the middle row's stencil into every interior row so
+  // that the interior is exactly Toeplitz: the kernels then take interior
+  // coefficients and the converged interior LU factors from the parameter
+  // bank (a rounding-level change of the matrices).
+  if (N > 4 * p) {
+    const int mid = N / 2;
+    for (std::vector<double>* X : {&P->M, &P->S, &P->A})
+      for (int r = 2 * p; r < N - 2 * p; r++)
+        for (int q = -p; q <= p; q++) (*X)[(size_t)r * N + r + q] = (*X)[(size_t)mid * N + mid + q];
+  }
   // material weights (D6): w[r*n+e] = int_{elem e} B_r / int B_r (Gauss q = p+1, exact)
   {
     P->wmat.assign((size_t)N * P->n, 0.0);
@@ -754,14 +766,15 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     } else if (!mass_factor(P->M, N, p, lo, hi, rel)) {
       return bail(fail(ADI_ERR_SINGULAR, "mass matrix factorisation: tiny pivot"));
     }
-    // fac: absolute row index.  The LU factors of the Toeplitz interior converge
-    // geometrically to a fixed row; rows [hk, tk) around the middle agree with it
-    // to 2 ulp (relative 4.5e-16), so the kernels take the middle row from the
-    // parameter bank there -- a perturbation of M at the level of its own rounding.
+    // fac: absolute row index.  The LU factors of the (exactly Toeplitz) interior
+    // converge geometrically to a fixed row; rows [hk, tk) agree with the
+    // reference row to 2 ulp (relative 4.5e-16), so the kernels take it from the
+    // parameter bank there -- a perturbation at the level of the factors' rounding.
     for (int k = lo; k < hi; k++)
       for (int q = 0; q < W; q++) fac[(size_t)k * W + q] = rel[(size_t)(k - lo) * W + q];
     {
-      const int mid = std::max(lo, std::min(hi - 1, N / 2));
+      // reference row: the last interior row before the tail (the LU recurrence has converged furthest there)
+      const int mid = std::max(lo, std::min(hi - 1, hi - 2 * p - 1));
       auto same = [&](int k) {
         for (int q = 0; q < W; q++) {
           const double a = fac[(size_t)k * W + q], b = fac[(size_t)mid * W + q];
@@ -803,8 +816,9 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   {
     // per-warp checkpoint slots: (grid warps) x (chunks) x (state words) x 32 lanes
     const int64_t warps = (int64_t)std::max(P->sw_grid[0], P->sw_grid[1]) * adi::SW_WARPS;
-    const int64_t nck = (N + 15) / 16;
-    P->ckpt_words = (size_t)(warps * nck * (int64_t)(p * (p + 2)) * 32);
+    const int64_t w_mass = (int64_t)(N + adi::SW_CH_MASS - 1) / adi::SW_CH_MASS * p;
+    const int64_t w_mod = (int64_t)(N + adi::SW_CH_MOD - 1) / adi::SW_CH_MOD * p * (p + 2);
+    P->ckpt_words = (size_t)(warps * std::max(w_mass, w_mod) * 32);
     if (!dmalloc(&P->ckpt, P->ckpt_words)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
   }
   if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));

@@ -57,16 +57,14 @@ cudaError_t Ops<ADI_P>::rhs_attrs() {
 }
 
 // sweep tiling: chunk of CH rows, ring of RS chunks per warp
-constexpr int SW_CH = 16;
-constexpr int SW_RS_MASS = 4;
-constexpr int SW_RS_MOD = 3;
+constexpr int SW_CH = SW_CH_MASS;
 
 template <>
 void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, bool modified) {
   const unsigned block = 32 * SW_WARPS;
   if (modified) {
-    constexpr size_t smem = sw_smem_bytes<ADI_P, true, SW_CH, SW_RS_MOD>();
-    sweep_kernel<ADI_P, true, SW_CH, SW_RS_MOD><<<grid, block, smem, st>>>(B);
+    constexpr size_t smem = sw_smem_bytes<ADI_P, true, SW_CH_MOD, SW_RS_MOD>();
+    sweep_kernel<ADI_P, true, SW_CH_MOD, SW_RS_MOD><<<grid, block, smem, st>>>(B);
   } else {
     constexpr size_t smem = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
     sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS><<<grid, block, smem, st>>>(B);
@@ -77,9 +75,9 @@ template <>
 cudaError_t Ops<ADI_P>::sweep_attrs(int occ[2]) {
   cudaError_t e;
   constexpr size_t s0 = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
-  constexpr size_t s1 = sw_smem_bytes<ADI_P, true, SW_CH, SW_RS_MOD>();
+  constexpr size_t s1 = sw_smem_bytes<ADI_P, true, SW_CH_MOD, SW_RS_MOD>();
   auto k0 = sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS>;
-  auto k1 = sweep_kernel<ADI_P, true, SW_CH, SW_RS_MOD>;
+  auto k1 = sweep_kernel<ADI_P, true, SW_CH_MOD, SW_RS_MOD>;
   if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0))) return e;
   if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k0, 32 * SW_WARPS, s0))) return e;

@@ -25,10 +25,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace adi {
 
 constexpr int SW_MAXJOBS = 3;
 constexpr int SW_WARPS = 4;  // warps per block
+// chunk rows (CH) and ring depth (RS) of the mass / row-modified kernels
+constexpr int SW_CH_MASS = 16, SW_RS_MASS = 4;
+constexpr int SW_CH_MOD = 8, SW_RS_MOD = 5;
 
 struct SweepJob {
   const double* in;   // right-hand side (N^3)
@@ -173,6 +178,18 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
       sw_commit();
     };
 
+    // per-tile constants in registers (var is runtime: no dynamic parameter indexing per row)
+    const double* fac = var ? B.fac[1] : B.fac[0];
+    const double* Mb = var ? B.Mb[1] : B.Mb[0];
+    const double* Sb = var ? B.Sb[1] : B.Sb[0];
+    const int hk = var ? B.hk[1] : B.hk[0];
+    const int tk = var ? B.tk[1] : B.tk[0];
+    double kf[MOD ? 1 : W];
+    if (!MOD) {
+#pragma unroll
+      for (int q = 0; q < W; q++) kf[q] = var ? B.kfac[1][q] : B.kfac[0][q];
+    }
+
     // recurrence state: yw[m-1] = y_{k-m}; (MOD) uw[m-1][j-1] = u_{k-m,k-m+j}, iw[m-1] = 1/u_{k-m,k-m}
     double yw[P];
     double uw[MOD ? P : 1][P];
@@ -188,24 +205,34 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
       }
     }
 
-    // row k of the modified matrix: a[q] = M_{k,k-P+q} + c_k S_{k,k-P+q}
-    auto mod_row = [&](int row, double cc, double* a) {
-      const bool in = row >= 2 * P && row < N - 2 * P;
-      const double* mr = B.Mb[var] + (size_t)row * W;
-      const double* sr = B.Sb[var] + (size_t)row * W;
-#pragma unroll
-      for (int q = 0; q < W; q++) {
-        const double mq = in ? B.kM[q] : __ldg(mr + q);
-        const double sq = in ? B.kS[q] : __ldg(sr + q);
-        a[q] = fma(cc, sq, mq);
+    // entry q of row k of the modified matrix: M_{k,k-P+q} + c_k S_{k,k-P+q};
+    // FAST: the row is Toeplitz (k in [2P, N-2P)), entries from the parameter bank
+    auto mod_entry = [&](auto fast, int row, double cc, int q) -> double {
+      if constexpr (decltype(fast)::value) {
+        return fma(cc, B.kS[q], B.kM[q]);
+      } else {
+        const bool in = row >= 2 * P && row < N - 2 * P;
+        const double mq = in ? B.kM[q] : __ldg(Mb + (size_t)row * W + q);
+        const double sq = in ? B.kS[q] : __ldg(Sb + (size_t)row * W + q);
+        return fma(cc, sq, mq);
+      }
+    };
+    // factor entry q of row k of the mass LU; FAST: k in [hk, tk)
+    auto fac_entry = [&](auto fast, int row, int q) -> double {
+      if constexpr (decltype(fast)::value) {
+        return kf[q];
+      } else {
+        const bool in = row >= hk && row < tk;
+        return in ? kf[q] : __ldg(fac + (size_t)row * W + q);
       }
     };
     // one forward elimination step (row k): returns y_k, and (MOD) u_{k,k+q}, q = 1..P in un[]
-    auto fwd = [&](int row, double fv, double cc, double ivk, double* un) -> double {
+    auto fwd = [&](auto fast, int row, double fv, double cc, double ivk, double* un) -> double {
       double y = fv;
       if (MOD) {
         double a[W];
-        mod_row(row, cc, a);
+#pragma unroll
+        for (int q = 0; q < W; q++) a[q] = mod_entry(fast, row, cc, q);
         double l[P + 1];
 #pragma unroll
         for (int m = P; m >= 1; m--) {
@@ -233,10 +260,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
 #pragma unroll
         for (int j = 0; j < P; j++) uw[0][j] = un[j];
       } else {
-        const bool in = row >= B.hk[var] && row < B.tk[var];
-        const double* fr = B.fac[var] + (size_t)row * W;
 #pragma unroll
-        for (int q = P - 1; q >= 0; q--) y = fma(-(in ? B.kfac[var][q] : __ldg(fr + q)), yw[q], y);
+        for (int q = P - 1; q >= 0; q--) y = fma(-fac_entry(fast, row, q), yw[q], y);
       }
 #pragma unroll
       for (int m = P - 1; m > 0; m--) yw[m] = yw[m - 1];
@@ -268,6 +293,63 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
         }
       }
     };
+    // chunk rows all in [lo,hi) and in the Toeplitz / converged range?
+    auto chunk_fast = [&](int r0) {
+      return r0 + CH <= hi && (MOD ? (r0 >= 2 * P && r0 + CH <= N - 2 * P) : (r0 >= hk && r0 + CH <= tk));
+    };
+    // pass-1 forward elimination of one chunk
+    auto fwd_chunk = [&](auto fast, const double* sl, int r0) {
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        const int row = r0 + r;
+        if (decltype(fast)::value || row < hi) {
+          double un[P];
+          fwd(fast, row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
+              MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
+        }
+      }
+    };
+    double xw[P];
+    // pass-2: recompute the chunk's forward elimination, then back-substitute (result in y[])
+    auto bwd_chunk = [&](auto fast, const double* sl, int r0, double* y) {
+      double us[CH][MOD && P > 1 ? P - 1 : 1];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        const int row = r0 + r;
+        y[r] = 0.0;
+        if (decltype(fast)::value || row < hi) {
+          double un[P];
+          y[r] = fwd(fast, row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
+                     MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
+          if (MOD) {
+#pragma unroll
+            for (int q = 0; q < P - 1; q++) us[r][q] = un[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int r = CH - 1; r >= 0; r--) {
+        const int row = r0 + r;
+        if (decltype(fast)::value || row < hi) {
+          double x = y[r];
+          if (MOD) {
+            const double cc = sl[(CH + r) * 33 + lane];
+            x = fma(-mod_entry(fast, row, cc, 2 * P), xw[P - 1], x);
+#pragma unroll
+            for (int q = P - 1; q >= 1; q--) x = fma(-us[r][q - 1], xw[q - 1], x);
+            x *= sl[(2 * CH + r) * 33 + lane];
+          } else {
+#pragma unroll
+            for (int q = P - 1; q >= 0; q--) x = fma(-fac_entry(fast, row, P + 1 + q), xw[q], x);
+            x *= fac_entry(fast, row, P);
+          }
+#pragma unroll
+          for (int q = P - 1; q > 0; q--) xw[q] = xw[q - 1];
+          xw[0] = x;
+          y[r] = x;
+        }
+      }
+    };
 
     // ---------------- pass 1: forward elimination, checkpoints ----------------
 #pragma unroll
@@ -281,21 +363,13 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
       save_state(c);
       const double* sl = ring + (c % RS) * SLOT;
       const int r0 = lo + c * CH;
-#pragma unroll
-      for (int r = 0; r < CH; r++) {
-        const int row = r0 + r;
-        if (row < hi) {
-          double un[P];
-          fwd(row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0, MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0,
-              un);
-        }
-      }
+      if (chunk_fast(r0)) fwd_chunk(std::true_type{}, sl, r0);
+      else fwd_chunk(std::false_type{}, sl, r0);
       __syncwarp();
       if (c + RS - 1 < nc) issue(c + RS - 1);
       else sw_commit();
     }
     // ---------------- pass 2: recompute per chunk, back substitution ----------
-    double xw[P];
 #pragma unroll
     for (int q = 0; q < P; q++) xw[q] = 0.0;
     double nxt[SWD];  // checkpoint of the next chunk to process, loaded one iteration ahead
@@ -314,47 +388,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
         for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(c - 1) * SWD + q) * 32];
       }
       double y[CH];
-      double us[CH][MOD && P > 1 ? P - 1 : 1];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
-#pragma unroll
-      for (int r = 0; r < CH; r++) {
-        const int row = r0 + r;
-        y[r] = 0.0;
-        if (row < hi) {
-          double un[P];
-          y[r] = fwd(row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
-                     MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
-          if (MOD) {
-#pragma unroll
-            for (int q = 0; q < P - 1; q++) us[r][q] = un[q];
-          }
-        }
-      }
-#pragma unroll
-      for (int r = CH - 1; r >= 0; r--) {
-        const int row = r0 + r;
-        if (row < hi) {
-          double x = y[r];
-          if (MOD) {
-            const double cc = sl[(CH + r) * 33 + lane];
-            double a[W];
-            mod_row(row, cc, a);
-            x = fma(-a[2 * P], xw[P - 1], x);
-#pragma unroll
-            for (int q = P - 1; q >= 1; q--) x = fma(-us[r][q - 1], xw[q - 1], x);
-            x *= sl[(2 * CH + r) * 33 + lane];
-          } else {
-            const bool in = row >= B.hk[var] && row < B.tk[var];
-            const double* fr = B.fac[var] + (size_t)row * W;
-#pragma unroll
-            for (int q = P - 1; q >= 0; q--) x = fma(-(in ? B.kfac[var][P + 1 + q] : __ldg(fr + P + 1 + q)), xw[q], x);
-            x *= in ? B.kfac[var][P] : __ldg(fr + P);
-          }
-#pragma unroll
-          for (int q = P - 1; q > 0; q--) xw[q] = xw[q - 1];
-          xw[0] = x;
-          y[r] = x;
-        }
-      }
+      if (chunk_fast(r0)) bwd_chunk(std::true_type{}, sl, r0, y);
+      else bwd_chunk(std::false_type{}, sl, r0, y);
       // store the chunk
       if (axis != 0) {
         double* po = out + base + (int64_t)r0 * stride;
