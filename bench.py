@@ -50,26 +50,33 @@ def dof_count(n: int, p: int) -> int:
 
 
 def algorithmic_bytes(n: int, p: int):
-    """Algorithmic HBM bytes per launch of each kernel class (DESIGN.md §Roofline).
+    """Algorithmic HBM bytes per launch of each kernel class (DESIGN.md §6).
 
     Units: U = N^3 coefficients; Ue = N (N-2)^2 active rows of an E component.
-      rhs_e      : 11 U * 8 B per substep (read E,H,a,c; write R), 3 launches/substep
-      rhs_h      : 13 U * 8 B per substep (read H,E^old,E^new,b; write G), 3 launches
-      sweep_mass : 16 B per active row (read rhs, write solution)
-      sweep_mod  : 24 B per active row (read rhs and c, write solution)
-    A sweep launch batches the three components (three jobs).  Per step: 4 mass
-    launches on E sets (3 x Ue rows each) + 6 on H sets (3 x U rows each); 2
-    row-modified launches on E sets (3 x Ue rows each).
+      rhs_e      : one component per launch: read E_d, H_{d+1}, H_{d+2}, E_sigma, a, c; write R_d -> 7 U * 8 B
+      rhs_h      : (general mu only) read H_d, Eo, En, b; write G_d -> 5 U * 8 B
+      sweep_mass : 16 B per active row (read rhs, write solution); 3 jobs per launch
+      sweep_mod  : 24 B per active row (read rhs and c, write solution); 3 jobs per launch
+      sweep_der  : 24 B per row (read u and base, write out); 3 jobs of U rows per launch
+    Per step with uniform mu: 4 mass launches on E sets, 2 row-modified, 4 derivative-projection.
     """
     N = n + p
     U = N ** 3
     Ue = N * (N - 2) ** 2
     return {
-        "rhs_e": 11 * U * 8 / 3.0,
-        "rhs_h": 13 * U * 8 / 3.0,
-        "sweep_mass": 16.0 * (12 * Ue + 18 * U) / 10.0,
+        "rhs_e": 7 * U * 8.0,
+        "rhs_h": 5 * U * 8.0,
+        "sweep_mass": 16.0 * 3 * Ue,
         "sweep_mod": 24.0 * 3 * Ue,
+        "sweep_der": 24.0 * 3 * U,
     }
+
+
+def step_bytes(n: int, p: int) -> float:
+    """Algorithmic HBM bytes of one step of the schedule run (uniform mu):
+    per substep 3 rhs_e (7U) + 1 mod + 2 mass launches (3 jobs each) + 2 derivative launches."""
+    a = algorithmic_bytes(n, p)
+    return 2 * (3 * a["rhs_e"] + a["sweep_mod"] + 2 * a["sweep_mass"] + 2 * a["sweep_der"])
 
 
 def hbm_peak():
@@ -311,8 +318,8 @@ def run_ours(args, cfg):
             kd["achieved_gbs"] = algo[k] / (t * 1e-3 / cnt) / 1e9
             kd["frac"] = kd["achieved_gbs"] / peak
         kernels[k] = kd
-    # end-to-end HBM fraction of the step (reference schedule, 168 B / DOF)
-    step_bytes = 126 * U * 8
+    # end-to-end HBM fraction of the step (algorithmic bytes of the schedule run)
+    sbytes = step_bytes(n, p)
     cpu = None
     if not args.no_cpu_baseline:
         rate, dt, desc = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)
@@ -324,7 +331,8 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": algo[cls]},
-        "step_hbm_frac": (step_bytes / (ms * 1e-3 / args.steps) / 1e9) / peak,
+        "step_hbm_frac": (sbytes / (ms * 1e-3 / args.steps) / 1e9) / peak,
+        "step_algorithmic_bytes": sbytes,
         "kernels": kernels,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -124,7 +124,7 @@ adi_status adi_synchronize(adi_patch patch);
 /* Number of full steps taken since creation. */
 int64_t adi_step_index(adi_patch patch);
 
-/* Number of kernel launches one adi_step(1) issues. */
+/* Number of kernel launches one adi_step(1) issues (known after the first adi_step). */
 int64_t adi_launches_per_step(adi_patch patch);
 
 /* The cudaStream_t the patch runs on. */
@@ -135,7 +135,8 @@ const char* adi_last_error(void);
 
 /* ---- per-kernel timing (bench instrumentation) -------------------------- */
 /* Kernel classes used by the timing report. */
-enum { ADI_K_RHS_E = 0, ADI_K_RHS_H = 1, ADI_K_SWEEP_MASS = 2, ADI_K_SWEEP_MOD = 3, ADI_K_OTHER = 4, ADI_K_NCLASS = 5 };
+enum { ADI_K_RHS_E = 0, ADI_K_RHS_H = 1, ADI_K_SWEEP_MASS = 2, ADI_K_SWEEP_MOD = 3, ADI_K_OTHER = 4,
+       ADI_K_SWEEP_DER = 5, ADI_K_NCLASS = 6 };
 
 /* enable != 0: subsequent adi_step calls launch kernels directly (no graph),
  * bracketing each launch with CUDA events on the patch stream; accumulated

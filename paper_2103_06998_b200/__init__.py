@@ -29,7 +29,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 ADI_OK, ADI_ERR_ARG, ADI_ERR_STATE, ADI_ERR_SINGULAR, ADI_ERR_CUDA, ADI_ERR_NCCL, ADI_ERR_OOM = range(7)
 ADI_BC_PEC, ADI_BC_NATURAL = 0, 1
-K_CLASSES = ["rhs_e", "rhs_h", "sweep_mass", "sweep_mod", "other"]
+K_CLASSES = ["rhs_e", "rhs_h", "sweep_mass", "sweep_mod", "other", "sweep_der"]
 
 EXPORTS = [
     "adi_create", "adi_destroy", "adi_layout", "adi_set_tau", "adi_set_materials", "adi_set_materials_tf",
@@ -239,8 +239,8 @@ class Patch:
         self._check(self._L.adi_set_timing(self.h, int(bool(enable))))
 
     def timing_report(self):
-        ms = (C.c_double * 5)()
-        n = (C.c_int64 * 5)()
+        ms = (C.c_double * len(K_CLASSES))()
+        n = (C.c_int64 * len(K_CLASSES))()
         self._check(self._L.adi_timing_report(self.h, ms, n))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(K_CLASSES)}
 

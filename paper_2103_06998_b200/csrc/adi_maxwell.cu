@@ -175,7 +175,10 @@ struct adi_patch_s {
   int hk[2] = {0, 0}, tk[2] = {0, 0};  // mass factor rows equal to the interior row
   std::vector<double> kfac[2];
   std::vector<double> kM, kS;          // interior Toeplitz rows of M, S
-  int sw_grid[2] = {0, 0};             // persistent grid of the mass / modified sweep
+  int sw_grid[3] = {0, 0, 0};          // persistent grid of the mass / modified / derivative sweep
+  bool mu_uniform = true;              // mu^ constant: H update by derivative projections (SURVEY §8(a) note)
+  double b_scalar = 0.0;               // tau / (2 mu^) when mu_uniform
+  int h_general = 0;                   // ADI_H_GENERAL=1: always the general H path (rhs_h + mass sweeps)
   double* load[3] = {};
   double* signal = nullptr;
   int64_t nsig = 0;
@@ -191,7 +194,7 @@ struct adi_patch_s {
   int64_t launches_per_step = 0;
   int64_t launch_counter = 0;
   int nsm = 148;
-  int sw_bps[2] = {0, 0};  // ADI_SW_BPS_MASS / ADI_SW_BPS_MOD: blocks per SM cap (0 = occupancy)
+  int sw_bps[3] = {0, 0, 0};  // ADI_SW_BPS_MASS / _MOD / _DER: blocks per SM cap (0 = occupancy)
   int use_tma = 0;   // RHS halo planes by TMA (N even, encoder available; ADI_RHS_CPA=1 disables)
 };
 
@@ -305,7 +308,7 @@ auto with_degree(int p, F&& f) {
 int rhs_kchunk(adi_patch P) {
   const int N = P->N;
   const int64_t tiles = (int64_t)((N + adi::RX_TX - 1) / adi::RX_TX) * ((N + adi::RX_TY - 1) / adi::RX_TY);
-  int kc = 64;
+  int kc = adi::RX_KCMAX;
   while (kc > 4 * P->p && tiles * ((N + kc - 1) / kc) < 4LL * P->nsm * 2) kc /= 2;
   return std::max(kc, 1);
 }
@@ -333,8 +336,12 @@ adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp
   bool tma = P->use_tma;
   const int nt = kind == 0 ? 4 : 3;
   for (int t = 0; t < nt && tma; t++) tma = make_field_map(&maps.m[t], args.u[t], N, P->p);
-  dim3 grid((N + adi::RX_TX - 1) / adi::RX_TX, (N + adi::RX_TY - 1) / adi::RX_TY, (N + args.kchunk - 1) / args.kchunk);
-  with_degree(P->p, [&](auto ops) { ops.rhs(P->stream, grid, args, maps, tma, kind, s, d); });
+  const int nch = (N + args.kchunk - 1) / args.kchunk;
+  dim3 grid((N + adi::RX_TX - 1) / adi::RX_TX, (N + adi::RX_TY - 1) / adi::RX_TY, nch);
+  // interior tiles (every output row Toeplitz in x and y): tiles 1 .. (N-2p)/T - 1
+  const int fx = std::max(0, (N - 2 * P->p) / adi::RX_TX - 1), fy = std::max(0, (N - 2 * P->p) / adi::RX_TY - 1);
+  dim3 gfast(fx, fy, fx && fy ? nch : 0);
+  with_degree(P->p, [&](auto ops) { ops.rhs(P->stream, grid, gfast, args, maps, tma, kind, s, d); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
@@ -375,7 +382,9 @@ struct SweepReq {
   int comp, axis;
   const double* in;
   double* out;
-  const double* iu;  // pivots of the family (modified)
+  const double* iu;      // pivots of the family (modified)
+  const double* base = nullptr;  // derivative projection: out = base + coef M^{-1} A in
+  double coef = 0.0;
 };
 
 adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
@@ -390,6 +399,8 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
     J.out = req[j].out;
     J.c = P->c;
     J.iu = req[j].iu;
+    J.base = req[j].base;
+    J.coef = req[j].coef;
     J.axis = req[j].axis;
     active_range(P, req[j].comp, req[j].axis, J.lo, J.hi);
     J.var = J.lo == 0 ? 0 : 1;
@@ -403,29 +414,31 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
     for (int q = 0; q < P->W; q++) B.kfac[v][q] = P->kfac[v][q];
   }
   for (int q = 0; q < P->W; q++) B.kM[q] = P->kM[q], B.kS[q] = P->kS[q];
+  B.Ab = P->d_tab + (size_t)adi::OP_A * P->N * P->W;
+  for (int q = 0; q < P->W; q++) B.kA[q] = P->tab_host[((size_t)adi::OP_A * P->N + P->N / 2) * P->W + q];
   return B;
 }
 
-adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, bool modified) {
+adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode) {
   adi::SweepBatch B = make_batch(P, req, nreq);
-  B.nck = (P->N + (modified ? adi::SW_CH_MOD : adi::SW_CH_MASS) - 1) / (modified ? adi::SW_CH_MOD : adi::SW_CH_MASS);
-  LaunchScope ls(P, modified ? ADI_K_SWEEP_MOD : ADI_K_SWEEP_MASS);
+  B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
+  LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
   const int64_t warps_needed = (int64_t)nreq * B.ntiles;
   const int64_t blocks_needed = (warps_needed + adi::SW_WARPS - 1) / adi::SW_WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[modified ? 1 : 0]);
-  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, modified); });
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[mode]);
+  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
 
 adi_status sweep_setup(adi_patch P) {
-  int occ[2] = {0, 0};
+  int occ[3] = {0, 0, 0};
   cudaError_t e = with_degree(P->p, [&](auto ops) { return ops.sweep_attrs(occ); });
-  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1) {
+  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1 || occ[2] < 1) {
     cudaGetLastError();
     return fail(ADI_ERR_CUDA, "sweep kernel attributes: %s", cudaGetErrorString(e));
   }
-  for (int m = 0; m < 2; m++) {
+  for (int m = 0; m < 3; m++) {
     int bps = occ[m];
     if (P->sw_bps[m] > 0) bps = std::min(bps, P->sw_bps[m]);
     P->sw_grid[m] = P->nsm * bps;
@@ -437,7 +450,7 @@ adi_status sweep_setup(adi_patch P) {
 // (may alias).  modified: M + diag(c) S per row (P:545/555/581), else M.
 adi_status sweep(adi_patch P, int comp, int axis, bool modified, const double* in, double* out, const double* iu) {
   SweepReq r{comp, axis, in, out, iu};
-  return launch_sweeps(P, &r, 1, modified);
+  return launch_sweeps(P, &r, 1, modified ? adi::SW_MOD : adi::SW_MASS);
 }
 
 // family index of the row-modified sweep of E component d in substep s
@@ -450,7 +463,7 @@ adi_status solve_e_range(adi_patch P, int s, int d0, int d1, const double* const
   SweepReq r[3];
   int n = 0;
   for (int d = d0; d < d1; d++) r[n++] = SweepReq{d, stiff_axis(s, d), in[d], out[d], P->iu[family(s, d)]};
-  adi_status st = launch_sweeps(P, r, n, true);
+  adi_status st = launch_sweeps(P, r, n, adi::SW_MOD);
   if (st) return st;
   for (int stage = 0; stage < 2; stage++) {
     n = 0;
@@ -461,7 +474,7 @@ adi_status solve_e_range(adi_patch P, int s, int d0, int d1, const double* const
         if (ax != sg) axes[k++] = ax;
       r[n++] = SweepReq{d, axes[stage], out[d], out[d], nullptr};
     }
-    if ((st = launch_sweeps(P, r, n, false))) return st;
+    if ((st = launch_sweeps(P, r, n, adi::SW_MASS))) return st;
   }
   return ADI_OK;
 }
@@ -479,9 +492,33 @@ adi_status solve_h_all(adi_patch P, double* const u[3]) {
   for (int ax = 0; ax < 3; ax++) {
     SweepReq r[3];
     for (int d = 0; d < 3; d++) r[d] = SweepReq{3 + d, ax, u[d], u[d], nullptr};
-    if ((st = launch_sweeps(P, r, 3, false))) return st;
+    if ((st = launch_sweeps(P, r, 3, adi::SW_MASS))) return st;
   }
   return ADI_OK;
+}
+
+// H update for uniform mu^ (b a scalar): M^{-3} G with G from discrete2 /
+// discrete4 (sign D2) collapses exactly to
+//   substep 1: H_D' = H_D - b D_{D+1} Eo_{D+2} + b D_{D+2} En_{D+1}
+//   substep 2: H_D' = H_D + b D_{D+2} Eo_{D+1} - b D_{D+1} En_{D+2}
+// with D_a = M_a^{-1} A_a along axis a (M^{-1}(M (x) A (x) M) = I (x) M^{-1}A (x) I;
+// H rows are unrestricted, PEC-eliminated E entries are stored zeros).  Two
+// batched derivative-projection launches (three components each).
+adi_status h_update_uniform_mu(adi_patch P, int s, const double* const H[3], const double* const Eo[3],
+                               const double* const En[3], double* const G[3]) {
+  const double b = P->b_scalar;
+  SweepReq r[3];
+  for (int d = 0; d < 3; d++) {
+    const int a1 = s == 1 ? (d + 1) % 3 : (d + 2) % 3, x1 = s == 1 ? (d + 2) % 3 : (d + 1) % 3;
+    r[d] = SweepReq{3 + d, a1, Eo[x1], G[d], nullptr, H[d], s == 1 ? -b : b};
+  }
+  adi_status st = launch_sweeps(P, r, 3, adi::SW_DER);
+  if (st) return st;
+  for (int d = 0; d < 3; d++) {
+    const int a2 = s == 1 ? (d + 2) % 3 : (d + 1) % 3, x2 = s == 1 ? (d + 1) % 3 : (d + 2) % 3;
+    r[d] = SweepReq{3 + d, a2, En[x2], G[d], nullptr, G[d], s == 1 ? b : -b};
+  }
+  return launch_sweeps(P, r, 3, adi::SW_DER);
 }
 
 // One substep (ALG-2 / ALG-7): RHS_E -> E solves -> RHS_H -> H solves, then
@@ -494,9 +531,13 @@ adi_status substep(adi_patch P, int s) {
     if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
   if ((st = solve_e_range(P, s, 0, 3, P->R, P->R))) return st;
   const double* En[3] = {P->R[0], P->R[1], P->R[2]};
-  for (int d = 0; d < 3; d++)
-    if ((st = rhs_h(P, s, d, H[d], E, En, P->G[d]))) return st;
-  if ((st = solve_h_all(P, P->G))) return st;
+  if (P->mu_uniform && !P->h_general) {
+    if ((st = h_update_uniform_mu(P, s, H, E, En, P->G))) return st;
+  } else {
+    for (int d = 0; d < 3; d++)
+      if ((st = rhs_h(P, s, d, H[d], E, En, P->G[d]))) return st;
+    if ((st = solve_h_all(P, P->G))) return st;
+  }
   for (int d = 0; d < 3; d++) {
     std::swap(P->F[d], P->R[d]);
     std::swap(P->F[3 + d], P->G[d]);
@@ -634,9 +675,25 @@ adi_status factorize(adi_patch P) {
   return st;
 }
 
+// a = tau/(2 eps^), b = tau/(2 mu^), c = tau^2/(4 eps^ mu^) (D13); detects
+// a uniform mu^ (then b is the scalar of the derivative-projection H update).
 adi_status derive_abc(adi_patch P, double* epsh, double* muh) {
+  drop_graph(P);  // kernel parameters (b, band constants) change with tau / materials
   adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh, muh, P->tau, P->U, P->a, P->b, P->c);
   CUDA_TRY(cudaGetLastError());
+  unsigned long long* mm;
+  CUDA_TRY(cudaMallocAsync(&mm, 2 * sizeof(unsigned long long), P->stream));
+  unsigned long long init[2] = {~0ull, 0ull}, h[2] = {0, 0};
+  CUDA_TRY(cudaMemcpyAsync(mm, init, sizeof init, cudaMemcpyHostToDevice, P->stream));
+  adi::minmax_pos_kernel<<<P->nsm * 4, 256, 0, P->stream>>>(muh, P->U, mm);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(h, mm, sizeof h, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaFreeAsync(mm, P->stream));
+  CUDA_TRY(cudaStreamSynchronize(P->stream));
+  P->mu_uniform = h[0] == h[1];
+  double mu0;
+  memcpy(&mu0, &h[0], sizeof mu0);
+  P->b_scalar = P->tau / (2.0 * mu0);
   return ADI_OK;
 }
 
@@ -702,6 +759,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   cudaDeviceGetAttribute(&P->nsm, cudaDevAttrMultiProcessorCount, cfg->device);
   if (const char* s = getenv("ADI_SW_BPS_MASS")) P->sw_bps[0] = atoi(s);
   if (const char* s = getenv("ADI_SW_BPS_MOD")) P->sw_bps[1] = atoi(s);
+  if (const char* s = getenv("ADI_SW_BPS_DER")) P->sw_bps[2] = atoi(s);
+  if (const char* s = getenv("ADI_H_GENERAL")) P->h_general = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   {
@@ -815,10 +874,11 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     if (!dmalloc(&P->iu[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc pivot caches"));
   {
     // per-warp checkpoint slots: (grid warps) x (chunks) x (state words) x 32 lanes
-    const int64_t warps = (int64_t)std::max(P->sw_grid[0], P->sw_grid[1]) * adi::SW_WARPS;
-    const int64_t w_mass = (int64_t)(N + adi::SW_CH_MASS - 1) / adi::SW_CH_MASS * p;
-    const int64_t w_mod = (int64_t)(N + adi::SW_CH_MOD - 1) / adi::SW_CH_MOD * p * (p + 2);
-    P->ckpt_words = (size_t)(warps * std::max(w_mass, w_mod) * 32);
+    int64_t words = 0;
+    for (int m = 0; m < 3; m++)
+      words = std::max<int64_t>(words, (int64_t)P->sw_grid[m] * adi::SW_WARPS * ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) *
+                                           adi::sw_state_words(m, p) * 32);
+    P->ckpt_words = (size_t)words;
     if (!dmalloc(&P->ckpt, P->ckpt_words)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
   }
   if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));
@@ -834,8 +894,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (e != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "setup: %s", cudaGetErrorString(e)));
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "setup: %s", cudaGetErrorString(e)));
-  // launches per step: 2 x (3 rhs_e + 3 batched E sweeps + 3 rhs_h + 3 batched H sweeps) + 1 counter kernel
-  P->launches_per_step = 2 * (3 + 3 + 3 + 3) + 1;
+  P->launches_per_step = 0;  // counted when the step is first recorded (adi_step)
   *out = P;
   return ADI_OK;
 }
@@ -1080,6 +1139,7 @@ adi_status adi_step(adi_patch P, int64_t k) {
       if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "capture: %s", cudaGetErrorString(e)));
       const int64_t lc = P->launch_counter;
       st = full_step(P);
+      P->launches_per_step = P->launch_counter - lc;
       P->launch_counter = lc;
       e = cudaStreamEndCapture(P->stream, &g);
       if (st) return poison(P, st);

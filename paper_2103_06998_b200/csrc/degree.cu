@@ -11,37 +11,45 @@ namespace adi {
 namespace {
 template <int KIND, int S, int D>
 struct RhsF {
-  static void run(cudaStream_t st, dim3 g, const RhsArgs& a, const RhsMaps& m, bool tma) {
+  static void run(cudaStream_t st, dim3 g, dim3 gf, const RhsArgs& a, const RhsMaps& m, bool tma) {
     constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-    if (tma) rhs_kernel<ADI_P, KIND, S, D, true><<<g, RX_THREADS, smem, st>>>(m, a);
-    else rhs_kernel<ADI_P, KIND, S, D, false><<<g, RX_THREADS, smem, st>>>(m, a);
+    if (tma) {
+      if (gf.x * gf.y) rhs_kernel<ADI_P, KIND, S, D, true, true><<<gf, RX_THREADS, smem, st>>>(m, a);
+      rhs_kernel<ADI_P, KIND, S, D, true, false><<<g, RX_THREADS, smem, st>>>(m, a);
+    } else {
+      if (gf.x * gf.y) rhs_kernel<ADI_P, KIND, S, D, false, true><<<gf, RX_THREADS, smem, st>>>(m, a);
+      rhs_kernel<ADI_P, KIND, S, D, false, false><<<g, RX_THREADS, smem, st>>>(m, a);
+    }
   }
 };
 template <int KIND, int S, int D>
 cudaError_t rhs_attr_one() {
   constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-  cudaError_t e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true, true>, A, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true, false>, A, (int)smem))) return e;
+  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false, true>, A, (int)smem))) return e;
+  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false, false>, A, (int)smem);
 }
 }  // namespace
 
 template <>
-void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind, int s,
-                     int d) {
+void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, dim3 gfast, const RhsArgs& args, const RhsMaps& maps, bool tma,
+                     int kind, int s, int d) {
   switch (kind * 6 + (s - 1) * 3 + d) {
-    case 0: RhsF<0, 1, 0>::run(st, grid, args, maps, tma); break;
-    case 1: RhsF<0, 1, 1>::run(st, grid, args, maps, tma); break;
-    case 2: RhsF<0, 1, 2>::run(st, grid, args, maps, tma); break;
-    case 3: RhsF<0, 2, 0>::run(st, grid, args, maps, tma); break;
-    case 4: RhsF<0, 2, 1>::run(st, grid, args, maps, tma); break;
-    case 5: RhsF<0, 2, 2>::run(st, grid, args, maps, tma); break;
-    case 6: RhsF<1, 1, 0>::run(st, grid, args, maps, tma); break;
-    case 7: RhsF<1, 1, 1>::run(st, grid, args, maps, tma); break;
-    case 8: RhsF<1, 1, 2>::run(st, grid, args, maps, tma); break;
-    case 9: RhsF<1, 2, 0>::run(st, grid, args, maps, tma); break;
-    case 10: RhsF<1, 2, 1>::run(st, grid, args, maps, tma); break;
-    default: RhsF<1, 2, 2>::run(st, grid, args, maps, tma); break;
+    case 0: RhsF<0, 1, 0>::run(st, grid, gfast, args, maps, tma); break;
+    case 1: RhsF<0, 1, 1>::run(st, grid, gfast, args, maps, tma); break;
+    case 2: RhsF<0, 1, 2>::run(st, grid, gfast, args, maps, tma); break;
+    case 3: RhsF<0, 2, 0>::run(st, grid, gfast, args, maps, tma); break;
+    case 4: RhsF<0, 2, 1>::run(st, grid, gfast, args, maps, tma); break;
+    case 5: RhsF<0, 2, 2>::run(st, grid, gfast, args, maps, tma); break;
+    case 6: RhsF<1, 1, 0>::run(st, grid, gfast, args, maps, tma); break;
+    case 7: RhsF<1, 1, 1>::run(st, grid, gfast, args, maps, tma); break;
+    case 8: RhsF<1, 1, 2>::run(st, grid, gfast, args, maps, tma); break;
+    case 9: RhsF<1, 2, 0>::run(st, grid, gfast, args, maps, tma); break;
+    case 10: RhsF<1, 2, 1>::run(st, grid, gfast, args, maps, tma); break;
+    default: RhsF<1, 2, 2>::run(st, grid, gfast, args, maps, tma); break;
   }
 }
 
@@ -56,32 +64,30 @@ cudaError_t Ops<ADI_P>::rhs_attrs() {
   return e;
 }
 
-// sweep tiling: chunk of CH rows, ring of RS chunks per warp
-constexpr int SW_CH = SW_CH_MASS;
-
 template <>
-void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, bool modified) {
+void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode) {
   const unsigned block = 32 * SW_WARPS;
-  if (modified) {
-    constexpr size_t smem = sw_smem_bytes<ADI_P, true, SW_CH_MOD, SW_RS_MOD>();
-    sweep_kernel<ADI_P, true, SW_CH_MOD, SW_RS_MOD><<<grid, block, smem, st>>>(B);
-  } else {
-    constexpr size_t smem = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
-    sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS><<<grid, block, smem, st>>>(B);
-  }
+  if (mode == SW_MOD) sweep_kernel<ADI_P, SW_MOD><<<grid, block, sw_smem_bytes<SW_MOD>(), st>>>(B);
+  else if (mode == SW_DER) sweep_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
+  else sweep_kernel<ADI_P, SW_MASS><<<grid, block, sw_smem_bytes<SW_MASS>(), st>>>(B);
 }
 
+namespace {
+template <int MODE>
+cudaError_t sweep_attr_one(int* occ) {
+  constexpr size_t smem = sw_smem_bytes<MODE>();
+  cudaError_t e = cudaFuncSetAttribute(sweep_kernel<ADI_P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<ADI_P, MODE>, 32 * SW_WARPS, smem);
+}
+}  // namespace
+
 template <>
-cudaError_t Ops<ADI_P>::sweep_attrs(int occ[2]) {
+cudaError_t Ops<ADI_P>::sweep_attrs(int occ[3]) {
   cudaError_t e;
-  constexpr size_t s0 = sw_smem_bytes<ADI_P, false, SW_CH, SW_RS_MASS>();
-  constexpr size_t s1 = sw_smem_bytes<ADI_P, true, SW_CH_MOD, SW_RS_MOD>();
-  auto k0 = sweep_kernel<ADI_P, false, SW_CH, SW_RS_MASS>;
-  auto k1 = sweep_kernel<ADI_P, true, SW_CH_MOD, SW_RS_MOD>;
-  if ((e = cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s0))) return e;
-  if ((e = cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k0, 32 * SW_WARPS, s0))) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k1, 32 * SW_WARPS, s1);
+  if ((e = sweep_attr_one<SW_MASS>(&occ[SW_MASS]))) return e;
+  if ((e = sweep_attr_one<SW_MOD>(&occ[SW_MOD]))) return e;
+  return sweep_attr_one<SW_DER>(&occ[SW_DER]);
 }
 
 template <>

@@ -16,13 +16,15 @@ template <int P>
 struct Ops {
   // RHS of the E (kind 0) / H (kind 1) system of component d in substep s.
   // tma: halo planes by cp.async.bulk.tensor (maps valid), else cp.async.
-  static void rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind, int s, int d);
+  // gfast: grid of the interior-tile launch (may be empty); grid: all tiles.
+  static void rhs(cudaStream_t st, dim3 grid, dim3 gfast, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind,
+                  int s, int d);
   static cudaError_t rhs_attrs();
   // One batched sweep launch (persistent grid chosen by the caller).
-  static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, bool modified);
-  // Set the dynamic shared memory of both sweep kernels; occ[0|1] = resident
-  // blocks per SM of the mass / modified kernel.
-  static cudaError_t sweep_attrs(int occ[2]);
+  static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode);
+  // Set the dynamic shared memory of the sweep kernels; occ[mode] = resident
+  // blocks per SM (SweepMode order: mass, modified, derivative projection).
+  static cudaError_t sweep_attrs(int occ[3]);
   // Pivot cache of one row-modified family (job 0 of B).
   static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };

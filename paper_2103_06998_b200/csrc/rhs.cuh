@@ -60,6 +60,7 @@ constexpr int RX_TY = 16;
 constexpr int RX_THREADS = 256;  // 32 x 8, two output rows each
 constexpr int RX_MAXT = 4;
 constexpr int RX_RING = 3;
+constexpr int RX_KCMAX = 64;  // max z-chunk (rows of the per-block z-coefficient table)
 
 struct RhsArgs {
   int N;
@@ -94,7 +95,8 @@ struct RxGeom {
 template <int P, int NT>
 __host__ __device__ constexpr size_t rhs_smem_bytes() {
   using G = RxGeom<P>;
-  return sizeof(double) * ((size_t)RX_RING * NT * G::PLANEP + (size_t)2 * NT * G::HY * RX_TX) +
+  return sizeof(double) * ((size_t)RX_RING * NT * G::PLANEP + (size_t)NT * G::HY * RX_TX +
+                           (size_t)3 * (RX_KCMAX + RX_TX + RX_TY) * (2 * P + 1)) +
          RX_RING * sizeof(uint64_t);
 }
 
@@ -132,9 +134,15 @@ __device__ __forceinline__ void rx_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void rx_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+
 // out[I] = sum_t sign_t * scale_t[I] * ((X_t (x) Y_t (x) Z_t) u_t)[I]  (- a s J),
 // zero outside the active set.
-template <int P, int KIND, int S, int D, bool TMA>
+// FAST: the tile is interior in x and y (every output row Toeplitz): x/y
+// coefficients come from the parameter bank; the general variant reads them
+// from per-block shared tables (rows of the band tables) and returns at once
+// for interior tiles (they are covered by the FAST launch).  z coefficients
+// always come from a per-block shared table (uniform broadcast reads).
+template <int P, int KIND, int S, int D, bool TMA, bool FAST>
 __global__ void __launch_bounds__(RX_THREADS, 2)
 rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs args) {
   using Prog = RhsProg<KIND, S, D>;
@@ -143,13 +151,22 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
   constexpr int W = G::W, HX = G::HX, HY = G::HY, PLANE = G::PLANE, PLANEP = G::PLANEP;
   extern __shared__ __align__(1024) double rx_smem[];
   double* ring = rx_smem;                                           // [RING][NT][PLANEP]
-  double* sx = rx_smem + RX_RING * NT * PLANEP;                     // [2][NT][HY][TX]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sx + 2 * NT * HY * RX_TX);  // [RING]
+  double* sx = rx_smem + RX_RING * NT * PLANEP;                     // [NT][HY][TX]
+  double* czs = sx + NT * HY * RX_TX;                               // [3][KCMAX][W]
+  double* cxs = czs + 3 * RX_KCMAX * W;                             // [3][TX][W]
+  double* cys = cxs + 3 * RX_TX * W;                                // [3][TY][W]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cys + 3 * RX_TY * W);  // [RING]
 
   const int N = args.N;
   const int tid = threadIdx.x;
   const int tx = tid & 31, ty = tid >> 5;  // y-pass / output: column tx, rows 2ty, 2ty+1
-  const int i0 = blockIdx.x * RX_TX, j0 = blockIdx.y * RX_TY;
+  const int bx = blockIdx.x + (FAST ? 1 : 0), by = blockIdx.y + (FAST ? 1 : 0);
+  const int i0 = bx * RX_TX, j0 = by * RX_TY;
+  if (!FAST) {
+    const bool xin = i0 >= 2 * P && i0 + RX_TX <= N - 2 * P;
+    const bool yin = j0 >= 2 * P && j0 + RX_TY <= N - 2 * P;
+    if (xin && yin) return;  // interior tile: the FAST launch owns it
+  }
   const int k0 = blockIdx.z * args.kchunk;
   const int k1 = min(N, k0 + args.kchunk);
   const int i = i0 + tx;
@@ -157,14 +174,27 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
   const int64_t NN = (int64_t)N * N;
   const int kbeg = k0 - P, kend = k1 + P;  // input planes [kbeg, kend)
 
-  if (TMA) {
-    if (tid == 0) {
-      for (int s = 0; s < RX_RING; s++) mbar_init(&bar[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    }
-    __syncthreads();
+  // per-block coefficient tables: rows of the band tables (0 outside [0,N))
+  for (int e = tid; e < 3 * (k1 - k0) * W; e += RX_THREADS) {
+    const int o = e / ((k1 - k0) * W), r = e - o * (k1 - k0) * W;
+    czs[o * RX_KCMAX * W + r] = args.tab[((int64_t)o * N + k0) * W + r];
   }
+  if (!FAST) {
+    for (int e = tid; e < 3 * RX_TX * W; e += RX_THREADS) {
+      const int o = e / (RX_TX * W), r = e - o * RX_TX * W, row = i0 + r / W;
+      cxs[e] = row < N ? args.tab[((int64_t)o * N + i0) * W + r] : 0.0;
+    }
+    for (int e = tid; e < 3 * RX_TY * W; e += RX_THREADS) {
+      const int o = e / (RX_TY * W), r = e - o * RX_TY * W, row = j0 + r / W;
+      cys[e] = row < N ? args.tab[((int64_t)o * N + j0) * W + r] : 0.0;
+    }
+  }
+  if (TMA && tid == 0) {
+    for (int s = 0; s < RX_RING; s++) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
   // producer of input plane kin into its ring slot
   auto produce = [&](int kin) {
     const int st = (kin - kbeg) % RX_RING;
@@ -210,7 +240,9 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
     const int64_t s = *args.step;
     if (s < args.nsig) sval = args.signal[s];
   }
-  const bool yin = jA >= 2 * P && jA + 1 < N - 2 * P;  // both output rows Toeplitz in y
+  const bool act_ij = i < N && i >= args.lo[0] && i < args.hi[0];
+  const int u = tid & 15;  // x-pass: outputs 2u, 2u+1 of rows (tid >> 4) + 16 m
+  const int xrow0 = tid >> 4;
 
   for (int g0 = kbeg; g0 < kend; g0 += W) {
 #pragma unroll
@@ -220,7 +252,7 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
         const int it = kin - kbeg;
         const int st = it % RX_RING;
         const double* slot = ring + st * NT * PLANEP;
-        double* sxb = sx + (it & 1) * NT * HY * RX_TX;
+        double* sxb = sx;
         // prefetch the row scales of the output plane k = kin - P
         const int k = kin - P;
         const bool kout = k >= k0 && i < N;
@@ -248,40 +280,32 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
         // ---- x-pass: rows yy of every term, two outputs (2u, 2u+1) per task
 #pragma unroll
         for (int t = 0; t < NT; t++) {
-          constexpr int dummy = 0;
-          (void)dummy;
           const int xop = Prog::op(t, 0);
-          for (int task = tid; task < HY * 16; task += RX_THREADS) {
-            const int yy = task >> 4, u = task & 15;
-            const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
-            double v[2 * P + 2];
 #pragma unroll
-            for (int q = 0; q <= P; q++) {
-              const double2 d2 = rp[q];
-              v[2 * q] = d2.x;
-              v[2 * q + 1] = d2.y;
-            }
-            const int x0 = i0 + 2 * u;
-            double o0 = 0.0, o1 = 0.0;
-            if (x0 >= 2 * P && x0 + 1 < N - 2 * P) {
+          for (int m = 0; m < (HY + 15) / 16; m++) {
+            const int yy = xrow0 + 16 * m;
+            if (m == 0 || yy < HY) {
+              const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
+              double v[2 * P + 2];
+#pragma unroll
+              for (int q = 0; q <= P; q++) {
+                const double2 d2 = rp[q];
+                v[2 * q] = d2.x;
+                v[2 * q + 1] = d2.y;
+              }
+              double o0 = 0.0, o1 = 0.0;
 #pragma unroll
               for (int q = 0; q < W; q++) {
-                o0 = fma(args.kint[xop][q], v[q], o0);
-                o1 = fma(args.kint[xop][q], v[q + 1], o1);
+                const double c0 = FAST ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u) * W + q];
+                const double c1 = FAST ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u + 1) * W + q];
+                o0 = fma(c0, v[q], o0);
+                o1 = fma(c1, v[q + 1], o1);
               }
-            } else {
-              const double* c0 = args.tab + ((int64_t)xop * N + x0) * W;
-              const bool ok0 = x0 < N, ok1 = x0 + 1 < N;
-#pragma unroll
-              for (int q = 0; q < W; q++) {
-                o0 = fma(ok0 ? __ldg(c0 + q) : 0.0, v[q], o0);
-                o1 = fma(ok1 ? __ldg(c0 + W + q) : 0.0, v[q + 1], o1);
-              }
+              *reinterpret_cast<double2*>(sxb + (t * HY + yy) * RX_TX + 2 * u) = make_double2(o0, o1);
             }
-            *reinterpret_cast<double2*>(sxb + (t * HY + yy) * RX_TX + 2 * u) = make_double2(o0, o1);
           }
         }
-        __syncthreads();  // x-pass(kin) visible; ring slot st free; y-pass(kin-1) used the other sx buffer
+        __syncthreads();  // x-pass(kin) visible; ring slot st free
         produce(kin + RX_RING);
         // ---- y-pass: rows 2ty, 2ty+1 of column tx -> z-window slot ph
 #pragma unroll
@@ -291,28 +315,21 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
 #pragma unroll
           for (int q = 0; q <= W; q++) col[q] = sxb[(t * HY + 2 * ty + q) * RX_TX + tx];
           double vA = 0.0, vB = 0.0;
-          if (yin) {
 #pragma unroll
-            for (int q = 0; q < W; q++) {
-              vA = fma(args.kint[yop][q], col[q], vA);
-              vB = fma(args.kint[yop][q], col[q + 1], vB);
-            }
-          } else {
-            const double* cA = args.tab + ((int64_t)yop * N + jA) * W;
-            const bool okA = jA < N, okB = jA + 1 < N;
-#pragma unroll
-            for (int q = 0; q < W; q++) {
-              vA = fma(okA ? __ldg(cA + q) : 0.0, col[q], vA);
-              vB = fma(okB ? __ldg(cA + W + q) : 0.0, col[q + 1], vB);
-            }
+          for (int q = 0; q < W; q++) {
+            const double cA = FAST ? args.kint[yop][q] : cys[(yop * RX_TY + 2 * ty) * W + q];
+            const double cB = FAST ? args.kint[yop][q] : cys[(yop * RX_TY + 2 * ty + 1) * W + q];
+            vA = fma(cA, col[q], vA);
+            vB = fma(cB, col[q + 1], vB);
           }
           w[t][0][ph] = vA;
           w[t][1][ph] = vB;
         }
+        __syncthreads();  // sx consumed: the next plane's x-pass may overwrite it
         // ---- z-pass + row scaling for the output plane k = kin - P
         if (kout) {
-          const bool zin = k >= 2 * P && k < N - 2 * P;
-          const bool ak = k >= args.lo[2] && k < args.hi[2] && i >= args.lo[0] && i < args.hi[0];
+          const bool ak = act_ij && k >= args.lo[2] && k < args.hi[2];
+          const double* zrow = czs + (k - k0) * W;
 #pragma unroll
           for (int r = 0; r < 2; r++) {
             const int j = jA + r;
@@ -322,14 +339,8 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
               for (int t = 0; t < NT; t++) {
                 const int zop = Prog::op(t, 2);
                 double z = 0.0;
-                if (zin) {
 #pragma unroll
-                  for (int q = 0; q < W; q++) z = fma(args.kint[zop][q], w[t][r][(ph + 1 + q) % W], z);
-                } else {
-                  const double* zc = args.tab + ((int64_t)zop * N + k) * W;
-#pragma unroll
-                  for (int q = 0; q < W; q++) z = fma(__ldg(zc + q), w[t][r][(ph + 1 + q) % W], z);
-                }
+                for (int q = 0; q < W; q++) z = fma(zrow[zop * RX_KCMAX * W + q], w[t][r][(ph + 1 + q) % W], z);
                 const int grp = Prog::scale(t) == SC_ONE ? 0 : Prog::scale(t) == SC_C ? 2 : 1;
                 zs[grp] = fma(Prog::sign(t), z, zs[grp]);
               }

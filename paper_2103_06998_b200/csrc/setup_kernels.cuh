@@ -68,4 +68,16 @@ __global__ void fill_kernel(double* __restrict__ x, int64_t n, double v) {
   for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) x[I] = v;
 }
 
+// min and max of a positive array (IEEE order of positive doubles = order of their bit patterns)
+__global__ void minmax_pos_kernel(const double* __restrict__ x, int64_t n, unsigned long long* mm) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long v = (unsigned long long)__double_as_longlong(x[I]);
+    lo = v < lo ? v : lo;
+    hi = v > hi ? v : hi;
+  }
+  atomicMin(&mm[0], lo);
+  atomicMax(&mm[1], hi);
+}
+
 }  // namespace adi

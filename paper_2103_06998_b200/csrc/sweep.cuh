@@ -14,8 +14,12 @@
 //           writes the solution.
 // HBM traffic is the algorithmic minimum: read f (and c, pivots), write x.
 //
+// Modes: SW_MASS solves M x = f; SW_MOD solves (M + diag(c) S) x = f; SW_DER
+// is the derivative projection of the uniform-mu H update (SURVEY §8(a)
+// note: M^{-1}(M (x) A (x) M) = I (x) M^{-1}A (x) I along the axis):
+//   out = base + coef * M^{-1} (A u)       (A applied on the fly, window +-P)
 // Constant (mass) matrix: precomputed LU factors; rows [hk, tk) equal the
-// interior factor row bit for bit and come from the kernel parameters.
+// interior factor row to 2 ulp and come from the kernel parameters.
 // Row-modified matrix M + diag(c) S (c = tau^2/(4 eps^ mu^) of the row's test
 // function): the pivots 1/u_kk are cached per fiber at set_materials/set_tau
 // (factor_kernel); the multipliers and the U row are recomputed from c in
@@ -31,15 +35,30 @@ namespace adi {
 
 constexpr int SW_MAXJOBS = 3;
 constexpr int SW_WARPS = 4;  // warps per block
-// chunk rows (CH) and ring depth (RS) of the mass / row-modified kernels
+enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
+// chunk rows (CH) and ring depth (RS) per mode
 constexpr int SW_CH_MASS = 16, SW_RS_MASS = 4;
 constexpr int SW_CH_MOD = 8, SW_RS_MOD = 5;
+constexpr int SW_CH_DER = 16, SW_RS_DER = 4;
+__host__ __device__ constexpr int sw_ch(int mode) { return mode == SW_MOD ? SW_CH_MOD : mode == SW_DER ? SW_CH_DER : SW_CH_MASS; }
+__host__ __device__ constexpr int sw_rs(int mode) { return mode == SW_MOD ? SW_RS_MOD : mode == SW_DER ? SW_RS_DER : SW_RS_MASS; }
+__host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? 3 : mode == SW_DER ? 2 : 1; }
+// checkpoint words per chunk: y window (P); MOD adds pivots (P) and U entries (P*P); DER adds the u window (P)
+__host__ __device__ constexpr int sw_state_words(int mode, int P) {
+  return mode == SW_MOD ? P * (P + 2) : mode == SW_DER ? 2 * P : P;
+}
+template <int MODE>
+constexpr size_t sw_smem_bytes() {
+  return sizeof(double) * (size_t)SW_WARPS * sw_rs(MODE) * sw_na(MODE) * sw_ch(MODE) * 33;
+}
 
 struct SweepJob {
-  const double* in;   // right-hand side (N^3)
-  double* out;        // solution (may equal in)
-  const double* c;    // per-test-function c (modified sweeps)
-  const double* iu;   // cached pivots 1/u_kk of this family (modified sweeps)
+  const double* in;   // right-hand side (MASS/MOD) or u (DER), N^3
+  double* out;        // solution (may equal in / base)
+  const double* c;    // per-test-function c (MOD)
+  const double* iu;   // cached pivots 1/u_kk of this family (MOD)
+  const double* base; // DER: out = base + coef * M^{-1} A u
+  double coef;
   int axis;           // 0 = x, 1 = y, 2 = z
   int lo, hi;         // active rows along the axis (PEC, D1)
   int var;            // band-table variant: 0 = [0,N), 1 = [1,N-1)
@@ -55,12 +74,15 @@ struct SweepBatch {
   // constant (mass) factors per variant: rows = absolute row index, W entries:
   //   [0..P-1] l_{k,k-1-q}, [P] 1/u_kk, [P+1..2P] u_{k,k+1+q}
   const double* fac[2];
-  int hk[2], tk[2];    // rows in [hk, tk) equal kfac bit for bit
+  int hk[2], tk[2];    // rows in [hk, tk) equal kfac to 2 ulp
   double kfac[2][11];
   // row-modified: band rows of M and S restricted to the variant's range
   const double* Mb[2];
   const double* Sb[2];
   double kM[11], kS[11];  // interior Toeplitz rows (rows in [2P, N-2P))
+  // derivative projection: band rows of A (full range) and its interior row
+  const double* Ab;
+  double kA[11];
 };
 
 __device__ __forceinline__ void sw_cp_async8(double* smem_dst, const double* gsrc) {
@@ -71,25 +93,15 @@ __device__ __forceinline__ void sw_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void sw_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int P, bool MOD, int CH>
-__host__ __device__ constexpr int sw_slot_doubles() {
-  return (MOD ? 3 : 1) * CH * 33;
-}
-template <int P, bool MOD, int CH, int RS>
-constexpr size_t sw_smem_bytes() {
-  return sizeof(double) * (size_t)SW_WARPS * RS * sw_slot_doubles<P, MOD, CH>();
-}
-template <int P, bool MOD>
-__host__ __device__ constexpr int sw_state_words() {
-  return MOD ? P * (P + 2) : P;
-}
-
-template <int P, bool MOD, int CH, int RS>
-__global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const __grid_constant__ SweepBatch B) {
+template <int P, int MODE>
+__global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_kernel(const __grid_constant__ SweepBatch B) {
+  constexpr bool MOD = MODE == SW_MOD, DER = MODE == SW_DER;
+  constexpr int CH = sw_ch(MODE), RS = sw_rs(MODE), NA = sw_na(MODE);
   constexpr int W = 2 * P + 1;
-  constexpr int NA = MOD ? 3 : 1;
-  constexpr int SLOT = sw_slot_doubles<P, MOD, CH>();
-  constexpr int SWD = sw_state_words<P, MOD>();
+  constexpr int SLOT = NA * CH * 33;
+  constexpr int SWD = sw_state_words(MODE, P);
+  constexpr int UW = MOD && P > 1 ? P - 1 : 1;  // stash width of U entries per row (pass 2)
+  static_assert(!DER || (RS >= 3 && CH >= P), "derivative mode needs the next chunk resident");
   extern __shared__ double sw_smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* ring = sw_smem + (size_t)wib * RS * SLOT;
@@ -105,13 +117,15 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
     const int tile = t - jb * B.ntiles;
     const double* src[3];
     double* out;
+    double coef;
     int axis, lo, hi, var;
     {
       const SweepJob& J = jb == 0 ? B.job[0] : jb == 1 ? B.job[1] : B.job[2];
       src[0] = J.in;
-      src[1] = J.c;
+      src[1] = DER ? J.base : J.c;
       src[2] = J.iu;
       out = J.out;
+      coef = J.coef;
       axis = J.axis;
       lo = J.lo;
       hi = J.hi;
@@ -138,26 +152,27 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
     const int xr = lane % CH, xf = lane / CH;
 
     // chunk c of the tile -> ring slot c % RS (layout [array][row][33], lane = fiber).
-    // Rows past hi are not loaded (the compute skips them).
-    auto issue = [&](int c) {
+    // Rows past hi are not loaded (the compute skips them).  na: arrays to load
+    // (DER loads `base` only in pass 2).
+    auto issue = [&](int c, int na) {
       double* sl = ring + (c % RS) * SLOT;
       const int r0 = lo + c * CH;
       const int nr = min(CH, hi - r0);
       if (axis != 0) {
-        const double* p0 = src[0] + base + (int64_t)r0 * stride;
-        const double* p1 = MOD ? src[1] + base + (int64_t)r0 * stride : nullptr;
-        const double* p2 = MOD ? src[2] + base + (int64_t)r0 * stride : nullptr;
+        const int64_t o = base + (int64_t)r0 * stride;
+        const double* p0 = src[0] + o;
+        const double* p1 = NA > 1 ? src[1] + o : nullptr;
+        const double* p2 = NA > 2 ? src[2] + o : nullptr;
 #pragma unroll
         for (int r = 0; r < CH; r++) {
           if (r < nr) {
             sw_cp_async8(sl + r * 33 + lane, p0);
-            if (MOD) {
-              sw_cp_async8(sl + (CH + r) * 33 + lane, p1);
-              sw_cp_async8(sl + (2 * CH + r) * 33 + lane, p2);
-            }
+            if (NA > 1 && (!DER || na > 1)) sw_cp_async8(sl + (CH + r) * 33 + lane, p1);
+            if (NA > 2) sw_cp_async8(sl + (2 * CH + r) * 33 + lane, p2);
           }
           p0 += stride;
-          if (MOD) p1 += stride, p2 += stride;
+          if (NA > 1) p1 += stride;
+          if (NA > 2) p2 += stride;
         }
       } else {
         const int row = min(r0 + xr, hi - 1);
@@ -169,10 +184,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
           const int64_t off = ff <= fmax ? o0 + (int64_t)N * ff : o0;
           double* d = sl + xr * 33 + ff;
           sw_cp_async8(d, src[0] + off);
-          if (MOD) {
-            sw_cp_async8(d + CH * 33, src[1] + off);
-            sw_cp_async8(d + 2 * CH * 33, src[2] + off);
-          }
+          if (NA > 1 && (!DER || na > 1)) sw_cp_async8(d + CH * 33, src[1] + off);
+          if (NA > 2) sw_cp_async8(d + 2 * CH * 33, src[2] + off);
         }
       }
       sw_commit();
@@ -190,10 +203,12 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
       for (int q = 0; q < W; q++) kf[q] = var ? B.kfac[1][q] : B.kfac[0][q];
     }
 
-    // recurrence state: yw[m-1] = y_{k-m}; (MOD) uw[m-1][j-1] = u_{k-m,k-m+j}, iw[m-1] = 1/u_{k-m,k-m}
+    // recurrence state: yw[m-1] = y_{k-m}; (MOD) uw[m-1][j-1] = u_{k-m,k-m+j}, iw[m-1] = 1/u_{k-m,k-m};
+    // (DER) dv[0..2P-1] = u_{k-P..k+P-1} before row k is eliminated
     double yw[P];
     double uw[MOD ? P : 1][P];
     double iw[MOD ? P : 1];
+    double dv[DER ? W : 1];
 #pragma unroll
     for (int m = 0; m < P; m++) yw[m] = 0.0;
     if (MOD) {
@@ -203,6 +218,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
 #pragma unroll
         for (int j = 0; j < P; j++) uw[m][j] = 0.0;
       }
+    }
+    if (DER) {
+#pragma unroll
+      for (int q = 0; q < W; q++) dv[q] = 0.0;
     }
 
     // entry q of row k of the modified matrix: M_{k,k-P+q} + c_k S_{k,k-P+q};
@@ -225,6 +244,22 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
         const bool in = row >= hk && row < tk;
         return in ? kf[q] : __ldg(fac + (size_t)row * W + q);
       }
+    };
+    // (DER) f_k = sum_q A_{k,k-P+q} u_{k-P+q} from the window dv
+    auto der_rhs = [&](auto fast, int row) -> double {
+      double fv = 0.0;
+#pragma unroll
+      for (int q = 0; q < W; q++) {
+        double aq;
+        if constexpr (decltype(fast)::value) {
+          aq = B.kA[q];
+        } else {
+          const bool in = row >= 2 * P && row < N - 2 * P;
+          aq = in ? B.kA[q] : __ldg(B.Ab + (size_t)row * W + q);
+        }
+        fv = fma(aq, dv[q], fv);
+      }
+      return fv;
     };
     // one forward elimination step (row k): returns y_k, and (MOD) u_{k,k+q}, q = 1..P in un[]
     auto fwd = [&](auto fast, int row, double fv, double cc, double ivk, double* un) -> double {
@@ -280,6 +315,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
           for (int j = 0; j < P; j++) p[(2 * P + m * P + j) * 32] = uw[m][j];
         }
       }
+      if (DER) {  // u_{r0-P..r0-1} = dv[0..P-1] at the chunk start
+#pragma unroll
+        for (int q = 0; q < P; q++) p[(P + q) * 32] = dv[q];
+      }
     };
     auto set_state = [&](const double* p) {
 #pragma unroll
@@ -292,41 +331,55 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
           for (int j = 0; j < P; j++) uw[m][j] = p[2 * P + m * P + j];
         }
       }
+      if (DER) {
+#pragma unroll
+        for (int q = 0; q < P; q++) dv[q] = p[P + q];
+      }
     };
     // chunk rows all in [lo,hi) and in the Toeplitz / converged range?
     auto chunk_fast = [&](int r0) {
-      return r0 + CH <= hi && (MOD ? (r0 >= 2 * P && r0 + CH <= N - 2 * P) : (r0 >= hk && r0 + CH <= tk));
+      return r0 + CH <= hi && (MOD || DER ? (r0 >= 2 * P && r0 + CH <= N - 2 * P) : true) &&
+             (MOD ? true : (r0 >= hk && r0 + CH <= tk));
     };
-    // pass-1 forward elimination of one chunk
-    auto fwd_chunk = [&](auto fast, const double* sl, int r0) {
-#pragma unroll
-      for (int r = 0; r < CH; r++) {
-        const int row = r0 + r;
-        if (decltype(fast)::value || row < hi) {
-          double un[P];
-          fwd(fast, row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
-              MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
-        }
-      }
+    // (DER) u at row r0+r of chunk slot sl, rows past the chunk from `nx` (next chunk) or `hd` (saved head)
+    auto der_u = [&](const double* sl, const double* nx, const double* hd, int r0, int r) -> double {
+      if (r0 + r >= hi) return 0.0;
+      if (r < CH) return sl[r * 33 + lane];
+      return nx ? nx[(r - CH) * 33 + lane] : hd[r - CH];
     };
+    // forward elimination of one chunk (pass 1 or the pass-2 recompute); y[] gets y_k,
+    // us[] (MOD) u_{k,k+q}, q = 1..P-1.  DER: dv holds u_{r0-P..r0+P-1} on entry
+    // (and u_{r0+CH-P..r0+CH+P-1} on exit).
     double xw[P];
-    // pass-2: recompute the chunk's forward elimination, then back-substitute (result in y[])
-    auto bwd_chunk = [&](auto fast, const double* sl, int r0, double* y) {
-      double us[CH][MOD && P > 1 ? P - 1 : 1];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
+    auto fwd_chunk = [&](auto fast, const double* sl, const double* nx, const double* hd, int r0, double* y,
+                         double* us) {
 #pragma unroll
       for (int r = 0; r < CH; r++) {
         const int row = r0 + r;
-        y[r] = 0.0;
         if (decltype(fast)::value || row < hi) {
           double un[P];
-          y[r] = fwd(fast, row, sl[r * 33 + lane], MOD ? sl[(CH + r) * 33 + lane] : 0.0,
-                     MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
-          if (MOD) {
+          double fv;
+          if (DER) {
+            // dv[0..2P-1] = u_{row-P..row+P-1} on entry: append u_{row+P}, apply A, slide
+            dv[W - 1] = der_u(sl, nx, hd, r0, r + P);
+            fv = der_rhs(fast, row);
 #pragma unroll
-            for (int q = 0; q < P - 1; q++) us[r][q] = un[q];
+            for (int q = 0; q < W - 1; q++) dv[q] = dv[q + 1];
+          } else {
+            fv = sl[r * 33 + lane];
+          }
+          const double yy = fwd(fast, row, fv, MOD ? sl[(CH + r) * 33 + lane] : 0.0,
+                                MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
+          if (y) y[r] = yy;
+          if (MOD && us) {
+#pragma unroll
+            for (int q = 0; q < P - 1; q++) us[r * UW + q] = un[q];
           }
         }
       }
+    };
+    // back substitution of one chunk (y[] -> x[] in place)
+    auto bwd_chunk = [&](auto fast, const double* sl, int r0, double* y, double* us) {
 #pragma unroll
       for (int r = CH - 1; r >= 0; r--) {
         const int row = r0 + r;
@@ -336,7 +389,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
             const double cc = sl[(CH + r) * 33 + lane];
             x = fma(-mod_entry(fast, row, cc, 2 * P), xw[P - 1], x);
 #pragma unroll
-            for (int q = P - 1; q >= 1; q--) x = fma(-us[r][q - 1], xw[q - 1], x);
+            for (int q = P - 1; q >= 1; q--) x = fma(-us[r * UW + q - 1], xw[q - 1], x);
             x *= sl[(2 * CH + r) * 33 + lane];
           } else {
 #pragma unroll
@@ -350,35 +403,56 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
         }
       }
     };
+    // DER: load u_{r0..r0+P-1} (the first P rows of the chunk) into dv[P..2P-1]
+    auto der_prime = [&](const double* sl, int r0) {
+#pragma unroll
+      for (int q = 0; q < P; q++) dv[P + q] = (r0 + q < hi) ? sl[q * 33 + lane] : 0.0;
+    };
 
     // ---------------- pass 1: forward elimination, checkpoints ----------------
+    // DER needs chunk c+1 resident while eliminating chunk c (window u_{k+P}).
+    constexpr int AHEAD = DER ? 1 : 0;
 #pragma unroll
     for (int c = 0; c < RS - 1; c++) {
-      if (c < nc) issue(c);
+      if (c < nc) issue(c, 1);
       else sw_commit();
     }
     for (int c = 0; c < nc; c++) {
-      sw_wait<RS - 2>();
+      sw_wait<RS - 2 - AHEAD>();
       __syncwarp();
-      save_state(c);
       const double* sl = ring + (c % RS) * SLOT;
+      const double* nx = (DER && c + 1 < nc) ? ring + ((c + 1) % RS) * SLOT : nullptr;
       const int r0 = lo + c * CH;
-      if (chunk_fast(r0)) fwd_chunk(std::true_type{}, sl, r0);
-      else fwd_chunk(std::false_type{}, sl, r0);
+      if (DER) der_prime(sl, r0);
+      save_state(c);
+      if (chunk_fast(r0)) fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+      else fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
       __syncwarp();
-      if (c + RS - 1 < nc) issue(c + RS - 1);
+      if (c + RS - 1 < nc) issue(c + RS - 1, 1);
       else sw_commit();
     }
+    sw_wait<0>();
+    __syncwarp();
     // ---------------- pass 2: recompute per chunk, back substitution ----------
+    // DER re-loads every chunk (u and base); MASS/MOD keep the last RS chunks of pass 1.
+    constexpr int KEEP = DER ? 0 : RS;
 #pragma unroll
     for (int q = 0; q < P; q++) xw[q] = 0.0;
-    double nxt[SWD];  // checkpoint of the next chunk to process, loaded one iteration ahead
+    double hd[DER ? P : 1];  // (DER) u of the first P rows of chunk c+1
+    double nxt[SWD];         // checkpoint of the next chunk to process, loaded one iteration ahead
 #pragma unroll
     for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(nc - 1) * SWD + q) * 32];
-    for (int c = nc - 1; c >= 0; c--) {
-      if (c < nc - RS) {  // not resident from pass 1: issued RS-1 iterations ago
-        sw_wait<RS - 2>();
+    if (DER) {
+#pragma unroll
+      for (int c = 0; c < RS - 1; c++) {
+        if (nc - 1 - c >= 0) issue(nc - 1 - c, 2);
+        else sw_commit();
       }
+#pragma unroll
+      for (int q = 0; q < P; q++) hd[q] = 0.0;
+    }
+    for (int c = nc - 1; c >= 0; c--) {
+      if (c < nc - KEEP) sw_wait<RS - 2>();  // issued RS-1 iterations ago
       __syncwarp();
       double* sl = ring + (c % RS) * SLOT;
       const int r0 = lo + c * CH;
@@ -387,9 +461,24 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
 #pragma unroll
         for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(c - 1) * SWD + q) * 32];
       }
+      if (DER) der_prime(sl, r0);
       double y[CH];
-      if (chunk_fast(r0)) bwd_chunk(std::true_type{}, sl, r0, y);
-      else bwd_chunk(std::false_type{}, sl, r0, y);
+      double us[CH * UW];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
+      if (chunk_fast(r0)) {
+        fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us);
+        bwd_chunk(std::true_type{}, sl, r0, y, us);
+      } else {
+#pragma unroll
+        for (int r = 0; r < CH; r++) y[r] = 0.0;
+        fwd_chunk(std::false_type{}, sl, nullptr, hd, r0, y, us);
+        bwd_chunk(std::false_type{}, sl, r0, y, us);
+      }
+      if (DER) {
+#pragma unroll
+        for (int q = 0; q < P; q++) hd[q] = (r0 + q < hi) ? sl[q * 33 + lane] : 0.0;
+#pragma unroll
+        for (int r = 0; r < CH; r++) y[r] = fma(coef, y[r], sl[(CH + r) * 33 + lane]);
+      }
       // store the chunk
       if (axis != 0) {
         double* po = out + base + (int64_t)r0 * stride;
@@ -399,6 +488,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
           po += stride;
         }
       } else {
+        __syncwarp();
 #pragma unroll
         for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
         __syncwarp();
@@ -411,9 +501,14 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MOD ? 1 : 3) sweep_kernel(const
         }
       }
       __syncwarp();
-      // ring slot (c+1)%RS is free (chunk c+1 done): fetch chunk c+1-RS into it
-      if (c < nc - 1 && c + 1 - RS >= 0) issue(c + 1 - RS);
-      else sw_commit();
+      // refill: MASS/MOD slot (c+1)%RS (chunk c+1 done) <- chunk c+1-RS; DER slot c%RS <- chunk c-(RS-1)
+      if (DER) {
+        if (c - (RS - 1) >= 0) issue(c - (RS - 1), 2);
+        else sw_commit();
+      } else {
+        if (c < nc - 1 && c + 1 - RS >= 0) issue(c + 1 - RS, 1);
+        else sw_commit();
+      }
     }
     sw_wait<0>();
     __syncwarp();

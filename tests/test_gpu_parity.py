@@ -226,7 +226,58 @@ def test_graph_and_direct_paths_agree():
     B.set_fields(f)
     B.step(3)
     rep = B.timing_report()
-    assert rep["sweep_mass"][1] == 3 * 2 * (2 + 3)  # batched: one launch per stage for all components
+    assert rep["sweep_mass"][1] == 3 * 2 * 2  # batched: one launch per stage for all components
     assert rep["sweep_mod"][1] == 3 * 2 * 1
+    assert rep["sweep_der"][1] == 3 * 2 * 2  # uniform mu: H by two derivative-projection launches
     for x, y in zip(A.get_fields(), B.get_fields()):
         assert np.array_equal(x, y)
+
+
+def _step_pair(n, p, tau, steps, eps_tf, mu_tf, general):
+    import os
+    old = os.environ.get("ADI_H_GENERAL")
+    os.environ["ADI_H_GENERAL"] = "1" if general else "0"
+    try:
+        G = adi.Patch(n, p, tau)
+    finally:
+        if old is None:
+            os.environ.pop("ADI_H_GENERAL")
+        else:
+            os.environ["ADI_H_GENERAL"] = old
+    O = oracle.Patch(n, p, tau)
+    f = workloads.random_fields(n + p, 21)
+    for X in (O, G):
+        X.set_materials_tf(eps_tf, mu_tf)
+        X.set_fields(f)
+        X.step(steps)
+    return [rel(a, b) for a, b in zip(G.get_fields(), O.get_fields())]
+
+
+@pytest.mark.parametrize("general", [False, True])
+def test_uniform_mu_h_paths(general):
+    """mu uniform (mu_r = 3): derivative-projection H update (default) and the general
+    rhs_h + mass-sweep path (ADI_H_GENERAL=1) both match the oracle."""
+    n, p = 11, 2
+    N = n + p
+    eps = workloads.random_tf(N, 8, 1.0, 80.0)
+    errs = _step_pair(n, p, 0.03, 3, eps, np.full(N ** 3, 3.0), general)
+    assert max(errs) <= TOL_STEP, errs
+
+
+def test_nonuniform_mu_general_path():
+    """Per-test-function mu varying: the general H path (rhs_h + mass sweeps) is taken."""
+    n, p = 9, 3
+    N = n + p
+    eps = workloads.random_tf(N, 9, 1.0, 80.0)
+    mu = workloads.random_tf(N, 10, 0.5, 2.0)
+    errs = _step_pair(n, p, 0.02, 3, eps, mu, False)
+    assert max(errs) <= TOL_STEP, errs
+
+
+@pytest.mark.parametrize("n,p", [(60, 2), (29, 3)])
+def test_derivative_projection_multi_chunk(n, p):
+    """H fast path over several 16-row chunks with a ragged tail, uniform mu."""
+    N = n + p
+    eps = workloads.random_tf(N, 11, 1.0, 80.0)
+    errs = _step_pair(n, p, 0.01, 2, eps, None, False)
+    assert max(errs) <= TOL_STEP, errs
