@@ -65,8 +65,8 @@ typedef struct {
   double tau;      /* time step, finite, > 0 */
   int32_t bc;      /* adi_bc; ADI_BC_PEC (D1) is the paper's Eq. (1) E x n = 0 */
   int32_t device;  /* CUDA device ordinal */
-  int32_t rank;    /* 0 (single GPU; distributed path reserved) */
-  int32_t nranks;  /* 1 */
+  int32_t rank;    /* this process's rank (0 for a single GPU) */
+  int32_t nranks;  /* 1: whole patch on this device; > 1: box-mode patch (see adi_box_*) */
   void* stream;    /* cudaStream_t to run on; NULL = a library-owned non-blocking stream */
 } adi_config;
 
@@ -159,6 +159,55 @@ adi_status adi_debug_rhs_e(adi_patch patch, int32_t s, double* const R[3]);
 adi_status adi_debug_rhs_h(adi_patch patch, int32_t s, const double* const Eo[3], const double* const En[3], double* const G[3]);
 /* E-component solve of substep s: stiffened sweep first, then the two mass sweeps. */
 adi_status adi_debug_solve_e(adi_patch patch, int32_t s, int32_t d, const double* rhs, double* out);
+
+/* ---- box-level entry points (slab-decomposed multi-GPU path) -------------
+ * SURVEY §8(e).  A patch created with nranks > 1 is a "box-mode" patch: it holds
+ * only the 1D operators (band tables, mass factors, interior constants) and the
+ * sweep checkpoints; the caller (paper_2103_06998_b200.dist) owns the slab buffers
+ * and drives the schedule -- halo exchange and all-to-all transposes between
+ * these calls go over NCCL via torch.distributed.  adi_layout gives the rank's
+ * z-slab [r N / R, (r+1) N / R).  All pointers are device pointers of the
+ * patch's device, arrays are x fastest; calls are asynchronous on the patch
+ * stream unless stated.  The single-patch calls (set_*, step, get_fields)
+ * return ADI_ERR_STATE on a box-mode patch. */
+typedef struct {
+  const double* in;   /* right-hand side (mass / modified) or u (derivative projection) */
+  double* out;        /* solution; may alias in (or base) */
+  const double* c;    /* modified: per-test-function c = tau^2/(4 eps^ mu^), same layout as in */
+  const double* iu;   /* modified: pivot cache from adi_box_factor for the same (comp, axis, layout) */
+  const double* base; /* derivative projection: out = base + coef * M^{-1} (A in) along axis */
+  double coef;
+  int64_t dims[3];    /* box extents; dims[axis] must equal N (fibers span the patch) */
+  int32_t axis;       /* 0 = x, 1 = y, 2 = z */
+  int32_t comp;       /* 0..5 (E1..H3): PEC row range along axis (D1) */
+} adi_sweep_job;
+
+/* 1..3 independent sweeps of one kind in one launch.  mode 0: M x = f; 1: (M + diag(c) S) x = f
+ * (no pivoting, D12); 2: derivative projection (uniform-mu H update, SURVEY §8(a) note). */
+adi_status adi_box_sweep(adi_patch patch, int32_t mode, int32_t njobs, const adi_sweep_job* jobs);
+/* Pivot cache 1/u_kk of the row-modified matrices of component comp along axis for a box
+ * layout (dims[axis] = N).  Synchronises; ADI_ERR_SINGULAR on a tiny pivot (D12 gate). */
+adi_status adi_box_factor(adi_patch patch, int32_t comp, int32_t axis, const int64_t dims[3], const double* c, double* iu);
+/* RHS of the E (kind 0, a1/a5) or H (kind 1, a3/a7) system of component d (0..2) in
+ * substep s (1|2) for output planes [kg0, kg0 + nzout) of the patch.  in[t]: the term
+ * inputs (order of the kernel programs: E: E_d, H_{d+2}, H_{d+1}, E_sigma; H: H_d, Eo, En),
+ * each N x N x nzin, plane zoff + k holding global plane kg0 + k (halo planes around it,
+ * zeros outside the patch); a, b, c, load: out layout; sval: source amplitude s((m+1/2)tau) (D9). */
+adi_status adi_box_rhs(adi_patch patch, int32_t kind, int32_t s, int32_t d, const double* const in[4], int64_t nzin,
+                       int64_t zoff, int64_t kg0, int64_t nzout, const double* a, const double* b, const double* c,
+                       const double* load, double sval, double* out);
+/* dst[doff + x] = src[soff + x] for x in the box ext (3D strided copy). */
+adi_status adi_box_copy(adi_patch patch, double* dst, const int64_t ddims[3], const int64_t doff[3], const double* src,
+                        const int64_t sdims[3], const int64_t soff[3], const int64_t ext[3]);
+/* Row factors a = tau/(2 eps^), b = tau/(2 mu^), c = tau^2/(4 eps^ mu^) of count entries. */
+adi_status adi_box_abc(adi_patch patch, const double* eps_tf, const double* mu_tf, int64_t count, double* a, double* b,
+                       double* c);
+/* Zero the PEC-eliminated entries (D1) of component comp held in a box at global offset off. */
+adi_status adi_box_pec(adi_patch patch, int32_t comp, double* u, const int64_t dims[3], const int64_t off[3]);
+/* Element-wise eps, mu (global n^3, host or device; mu NULL => 1) -> per-test-function
+ * eps^, mu^ (global N^3 device arrays, D6).  Synchronises. */
+adi_status adi_box_materials_tf(adi_patch patch, const double* eps_elem, const double* mu_elem, double* eps_tf,
+                                double* mu_tf);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "lib", "libadimaxwell.so")
+# ADI_LIB selects another build of the library (tuning experiments); default: the in-tree build
+LIB_PATH = os.environ.get("ADI_LIB") or os.path.join(_HERE, "lib", "libadimaxwell.so")
 CSRC = os.path.join(_HERE, "csrc")
 SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh")] + [
     os.path.join(_ROOT, "include", "adi_maxwell.h")]
@@ -37,40 +38,50 @@ EXPORTS = [
     "adi_step_index", "adi_launches_per_step", "adi_stream", "adi_last_error", "adi_set_timing",
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
+    "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
+    "adi_box_materials_tf",
 ]
 
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, lib_path: str | None = None, extra_flags=()) -> str:
     """Compile libadimaxwell.so in-tree for sm_100a (nvcc; no GPU needed).
 
     One object per B-spline degree (csrc/degree.cu with -DADI_P=p) plus the host
     orchestration (csrc/adi_maxwell.cu), compiled in parallel, then linked."""
-    os.makedirs(os.path.dirname(LIB_PATH), exist_ok=True)
+    lib_path = lib_path or LIB_PATH
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     newest = max(os.path.getmtime(s) for s in SOURCES)
-    if not (force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest):
-        return LIB_PATH
-    objdir = os.path.join(os.path.dirname(LIB_PATH), "obj")
+    if not (force or not os.path.exists(lib_path) or os.path.getmtime(lib_path) < newest):
+        return lib_path
+    objdir = os.path.join(os.path.dirname(lib_path), "obj")
     os.makedirs(objdir, exist_ok=True)
     jobs = [(os.path.join(objdir, "adi_maxwell.o"), [os.path.join(CSRC, "adi_maxwell.cu")])]
     for p in DEGREES:
         jobs.append((os.path.join(objdir, f"degree_p{p}.o"), [f"-DADI_P={p}", os.path.join(CSRC, "degree.cu")]))
     procs = []
     for obj, args in jobs:
-        cmd = ["nvcc", *NVCC_FLAGS, "-c", "-o", obj, *args]
+        cmd = ["nvcc", *NVCC_FLAGS, *extra_flags, "-c", "-o", obj, *args]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((cmd, subprocess.Popen(cmd)))
     bad = [cmd for cmd, pr in procs if pr.wait() != 0]
     if bad:
         raise RuntimeError("nvcc failed: " + " | ".join(" ".join(c) for c in bad))
-    tmp = LIB_PATH + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *[o for o, _ in jobs]]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
+
+
+class SweepJob(C.Structure):
+    """adi_sweep_job (include/adi_maxwell.h)."""
+    _fields_ = [("in_", C.c_void_p), ("out", C.c_void_p), ("c", C.c_void_p), ("iu", C.c_void_p),
+                ("base", C.c_void_p), ("coef", C.c_double), ("dims", C.c_int64 * 3), ("axis", C.c_int32),
+                ("comp", C.c_int32)]
 
 
 class AdiConfig(C.Structure):
@@ -120,6 +131,17 @@ def lib():
             L.adi_debug_rhs_e.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
             L.adi_debug_rhs_h.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
             L.adi_debug_solve_e.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+            i64x3 = C.POINTER(C.c_int64)
+            L.adi_box_sweep.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(SweepJob)]
+            L.adi_box_factor.argtypes = [C.c_void_p, C.c_int32, C.c_int32, i64x3, C.c_void_p, C.c_void_p]
+            L.adi_box_rhs.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
+                                      C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_double, C.c_void_p]
+            L.adi_box_copy.argtypes = [C.c_void_p, C.c_void_p, i64x3, i64x3, C.c_void_p, i64x3, i64x3, i64x3]
+            L.adi_box_abc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
+            L.adi_box_pec.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, i64x3, i64x3]
+            L.adi_box_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             _lib = L
         return _lib
 
@@ -156,10 +178,11 @@ def _ptr_array(objs):
 class Patch:
     """One n x n x n patch on one B200 (device memory owned by the library)."""
 
-    def __init__(self, n: int, p: int, tau: float, bc: int = ADI_BC_PEC, device: int = 0):
+    def __init__(self, n: int, p: int, tau: float, bc: int = ADI_BC_PEC, device: int = 0, rank: int = 0,
+                 nranks: int = 1, stream: int | None = None):
         L = lib()
         self._L = L
-        cfg = AdiConfig(int(n), int(p), float(tau), int(bc), int(device), 0, 1, None)
+        cfg = AdiConfig(int(n), int(p), float(tau), int(bc), int(device), int(rank), int(nranks), stream)
         h = C.c_void_p()
         self._check(L.adi_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -243,6 +266,59 @@ class Patch:
         n = (C.c_int64 * len(K_CLASSES))()
         self._check(self._L.adi_timing_report(self.h, ms, n))
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(K_CLASSES)}
+
+    def layout(self):
+        """(N, k0, k1): this rank's z-slab [k0, k1) of the N^3 grid."""
+        N, k0, k1 = C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self._L.adi_layout(self.h, C.byref(N), C.byref(k0), C.byref(k1)))
+        return N.value, k0.value, k1.value
+
+    # ---- box-level calls (slab-decomposed path; torch CUDA tensors) ---------------
+    @staticmethod
+    def _i3(v):
+        return (C.c_int64 * 3)(*[int(x) for x in v])
+
+    def box_sweep(self, mode: int, jobs):
+        """jobs: list of dicts with keys in, out, dims, axis, comp [, c, iu, base, coef]."""
+        arr = (SweepJob * len(jobs))()
+        for a, j in zip(arr, jobs):
+            a.in_ = _addr(j["in"])
+            a.out = _addr(j["out"])
+            a.c = _addr(j["c"]) if j.get("c") is not None else None
+            a.iu = _addr(j["iu"]) if j.get("iu") is not None else None
+            a.base = _addr(j["base"]) if j.get("base") is not None else None
+            a.coef = float(j.get("coef", 0.0))
+            a.dims = (C.c_int64 * 3)(*[int(x) for x in j["dims"]])
+            a.axis = int(j["axis"])
+            a.comp = int(j["comp"])
+        self._check(self._L.adi_box_sweep(self.h, int(mode), len(jobs), arr))
+
+    def box_factor(self, comp: int, axis: int, dims, c, iu):
+        self._check(self._L.adi_box_factor(self.h, int(comp), int(axis), self._i3(dims), _addr(c), _addr(iu)))
+
+    def box_rhs(self, kind: int, s: int, d: int, ins, nzin: int, zoff: int, kg0: int, nzout: int, a, b, c, load,
+                sval: float, out):
+        self._check(self._L.adi_box_rhs(self.h, int(kind), int(s), int(d), _ptr_array(list(ins) + [None] * (4 - len(ins))),
+                                        int(nzin), int(zoff), int(kg0), int(nzout),
+                                        None if a is None else _addr(a), None if b is None else _addr(b),
+                                        None if c is None else _addr(c), None if load is None else _addr(load),
+                                        float(sval), _addr(out)))
+
+    def box_copy(self, dst, ddims, doff, src, sdims, soff, ext):
+        self._check(self._L.adi_box_copy(self.h, _addr(dst), self._i3(ddims), self._i3(doff), _addr(src),
+                                         self._i3(sdims), self._i3(soff), self._i3(ext)))
+
+    def box_abc(self, eps_tf, mu_tf, count: int, a, b, c):
+        self._check(self._L.adi_box_abc(self.h, _addr(eps_tf), _addr(mu_tf), int(count), _addr(a), _addr(b), _addr(c)))
+
+    def box_pec(self, comp: int, u, dims, off):
+        self._check(self._L.adi_box_pec(self.h, int(comp), _addr(u), self._i3(dims), self._i3(off)))
+
+    def box_materials_tf(self, eps_elem, mu_elem, eps_tf, mu_tf):
+        e = _as_f64(eps_elem)
+        m = None if mu_elem is None else _as_f64(mu_elem)
+        self._check(self._L.adi_box_materials_tf(self.h, _addr(e), None if m is None else _addr(m), _addr(eps_tf),
+                                                 _addr(mu_tf)))
 
     # ---- test-only -------------------------------------------------------------
     def matrices(self):

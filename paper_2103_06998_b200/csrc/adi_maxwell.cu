@@ -279,10 +279,10 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 
 // 3D map of an N^3 fp64 field (x fastest) with a (32+2P) x (16+2P) x 1 box;
 // out-of-bounds elements are zero-filled (the halo outside the patch).
-bool make_field_map(CUtensorMap* m, const double* ptr, int N, int p) {
+bool make_field_map(CUtensorMap* m, const double* ptr, int N, int nz, int p) {
   auto enc = tma_encoder();
-  if (!enc || (N & 1)) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)N};
+  if (!enc || (N & 1) || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)N, (cuuint64_t)nz};
   cuuint64_t strides[2] = {(cuuint64_t)N * 8, (cuuint64_t)N * N * 8};
   cuuint32_t box[3] = {(cuuint32_t)(adi::RX_TX + 2 * p), (cuuint32_t)(adi::RX_TY + 2 * p), 1};
   cuuint32_t es[3] = {1, 1, 1};
@@ -305,17 +305,21 @@ auto with_degree(int p, F&& f) {
 }
 
 // z-chunk length: enough blocks to fill the machine (>= ~4 waves of 2 blocks/SM), halo <= 25%
-int rhs_kchunk(adi_patch P) {
+int rhs_kchunk(adi_patch P, int nz) {
   const int N = P->N;
   const int64_t tiles = (int64_t)((N + adi::RX_TX - 1) / adi::RX_TX) * ((N + adi::RX_TY - 1) / adi::RX_TY);
   int kc = adi::RX_KCMAX;
-  while (kc > 4 * P->p && tiles * ((N + kc - 1) / kc) < 4LL * P->nsm * 2) kc /= 2;
+  while (kc > 4 * P->p && tiles * ((nz + kc - 1) / kc) < 4LL * P->nsm * 2) kc /= 2;
   return std::max(kc, 1);
 }
 
 adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp, int cls) {
   args.N = P->N;
-  args.kchunk = rhs_kchunk(P);
+  if (args.nzin == 0) {  // whole patch (single-GPU path)
+    args.nzin = args.nzout = P->N;
+    args.zoff = args.kg0 = 0;
+  }
+  args.kchunk = rhs_kchunk(P, args.nzout);
   args.tab = P->d_tab;
   args.a = P->a;
   args.b = P->b;
@@ -335,8 +339,8 @@ adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp
   memset(&maps, 0, sizeof maps);
   bool tma = P->use_tma;
   const int nt = kind == 0 ? 4 : 3;
-  for (int t = 0; t < nt && tma; t++) tma = make_field_map(&maps.m[t], args.u[t], N, P->p);
-  const int nch = (N + args.kchunk - 1) / args.kchunk;
+  for (int t = 0; t < nt && tma; t++) tma = make_field_map(&maps.m[t], args.u[t], N, args.nzin, P->p);
+  const int nch = (args.nzout + args.kchunk - 1) / args.kchunk;
   dim3 grid((N + adi::RX_TX - 1) / adi::RX_TX, (N + adi::RX_TY - 1) / adi::RX_TY, nch);
   // interior tiles (every output row Toeplitz in x and y): tiles 1 .. (N-2p)/T - 1
   const int fx = std::max(0, (N - 2 * P->p) / adi::RX_TX - 1), fy = std::max(0, (N - 2 * P->p) / adi::RX_TY - 1);
@@ -385,16 +389,22 @@ struct SweepReq {
   const double* iu;      // pivots of the family (modified)
   const double* base = nullptr;  // derivative projection: out = base + coef M^{-1} A in
   double coef = 0.0;
+  int64_t dims[3] = {0, 0, 0};   // box extents (x fastest); 0 = the whole N^3 patch
 };
 
 adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
   adi::SweepBatch B{};
   B.N = P->N;
   B.njobs = nreq;
-  B.ntiles = (int)(((int64_t)P->N * P->N + 31) / 32);
   B.ckpt = P->ckpt;
+  int64_t tiles = 0;
   for (int j = 0; j < nreq; j++) {
     adi::SweepJob& J = B.job[j];
+    for (int a = 0; a < 3; a++) J.dims[a] = req[j].dims[a] ? (int)req[j].dims[a] : P->N;
+    const int ax = req[j].axis;
+    const int64_t nfib = (int64_t)J.dims[(ax + 1) % 3] * J.dims[(ax + 2) % 3];
+    J.tile0 = (int)tiles;
+    tiles += (nfib + 31) / 32;
     J.in = req[j].in;
     J.out = req[j].out;
     J.c = P->c;
@@ -405,6 +415,7 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
     active_range(P, req[j].comp, req[j].axis, J.lo, J.hi);
     J.var = J.lo == 0 ? 0 : 1;
   }
+  B.ntiles = (int)tiles;
   for (int v = 0; v < 2; v++) {
     B.fac[v] = P->d_fac[v];
     B.Mb[v] = P->d_Mb[v];
@@ -423,7 +434,7 @@ adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode) {
   adi::SweepBatch B = make_batch(P, req, nreq);
   B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
   LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
-  const int64_t warps_needed = (int64_t)nreq * B.ntiles;
+  const int64_t warps_needed = B.ntiles;
   const int64_t blocks_needed = (warps_needed + adi::SW_WARPS - 1) / adi::SW_WARPS;
   const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[mode]);
   with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode); });
@@ -651,7 +662,7 @@ adi_status factor_into(adi_patch P, int comp, int axis, double* iu, unsigned lon
   adi::SweepBatch B = make_batch(P, &r, 1);
   unsigned long long init = ~0ull;
   CUDA_TRY(cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream));
-  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)P->N * P->N + 127) / 128, (int64_t)P->nsm * 8);
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)B.ntiles * 32 + 127) / 128, (int64_t)P->nsm * 8);
   with_degree(P->p, [&](auto ops) { ops.factor(P->stream, grid, B, iu, bad, 1e-14); });
   CUDA_TRY(cudaGetLastError());
   unsigned long long h = 0;
@@ -732,8 +743,10 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (cfg->p < 1 || cfg->p > 5) return fail(ADI_ERR_ARG, "adi_create: p = %d outside 1..5", cfg->p);
   if (!(cfg->tau > 0.0) || !std::isfinite(cfg->tau)) return fail(ADI_ERR_ARG, "adi_create: tau must be finite and > 0");
   if (cfg->bc != ADI_BC_PEC && cfg->bc != ADI_BC_NATURAL) return fail(ADI_ERR_ARG, "adi_create: bad bc %d", cfg->bc);
-  if (cfg->nranks != 1 || cfg->rank != 0)
-    return fail(ADI_ERR_ARG, "adi_create: this build is single-rank (rank 0 of 1)");
+  if (cfg->nranks < 1 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+    return fail(ADI_ERR_ARG, "adi_create: rank %d of %d", cfg->rank, cfg->nranks);
+  if (cfg->nranks > cfg->n + cfg->p)
+    return fail(ADI_ERR_ARG, "adi_create: %d ranks for %d planes", cfg->nranks, cfg->n + cfg->p);
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) return fail(ADI_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(e));
   adi_patch P = new adi_patch_s();
@@ -857,12 +870,16 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     cudaMemcpy(P->d_Mb[var], Mb.data(), Mb.size() * sizeof(double), cudaMemcpyHostToDevice);
     cudaMemcpy(P->d_Sb[var], Sb.data(), Sb.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
-  const size_t U = (size_t)P->U;
-  for (int i = 0; i < 6; i++)
+  // box mode (nranks > 1): the caller owns the slab buffers (adi_box_*); the patch
+  // keeps only the 1D operators, factor tables and sweep checkpoints.
+  const bool whole = cfg->nranks == 1;
+  const size_t U = whole ? (size_t)P->U : 0;
+  for (int i = 0; i < 6 && whole; i++)
     if (!dmalloc(&P->F[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc fields (%zu doubles)", U));
-  for (int i = 0; i < 3; i++)
+  for (int i = 0; i < 3 && whole; i++)
     if (!dmalloc(&P->R[i], U) || !dmalloc(&P->G[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc scratch fields"));
-  if (!dmalloc(&P->a, U) || !dmalloc(&P->b, U) || !dmalloc(&P->c, U) || !dmalloc(&P->epsh, U) || !dmalloc(&P->muh, U))
+  if (whole &&
+      (!dmalloc(&P->a, U) || !dmalloc(&P->b, U) || !dmalloc(&P->c, U) || !dmalloc(&P->epsh, U) || !dmalloc(&P->muh, U)))
     return bail(fail(ADI_ERR_OOM, "cudaMalloc material arrays"));
   P->kM.assign(11, 0.0);
   P->kS.assign(11, 0.0);
@@ -870,7 +887,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     P->kM[q] = tab[((size_t)adi::OP_M * N + N / 2) * W + q];
     P->kS[q] = tab[((size_t)adi::OP_S * N + N / 2) * W + q];
   }
-  for (int i = 0; i < 6; i++)
+  for (int i = 0; i < 6 && whole; i++)
     if (!dmalloc(&P->iu[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc pivot caches"));
   {
     // per-warp checkpoint slots: (grid warps) x (chunks) x (state words) x 32 lanes
@@ -883,13 +900,15 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   }
   if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));
   cudaMemset(P->d_step, 0, sizeof(int64_t));
-  for (int i = 0; i < 6; i++) cudaMemset(P->F[i], 0, U * sizeof(double));
-  // eps = mu = 1
-  adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->epsh, P->U, 1.0);
-  adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->muh, P->U, 1.0);
-  adi_status st = derive_abc(P, P->epsh, P->muh);
-  if (!st) st = factorize(P);
-  if (st) return bail(st);
+  if (whole) {
+    for (int i = 0; i < 6; i++) cudaMemset(P->F[i], 0, U * sizeof(double));
+    // eps = mu = 1
+    adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->epsh, P->U, 1.0);
+    adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->muh, P->U, 1.0);
+    adi_status st = derive_abc(P, P->epsh, P->muh);
+    if (!st) st = factorize(P);
+    if (st) return bail(st);
+  }
   e = cudaStreamSynchronize(P->stream);
   if (e != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "setup: %s", cudaGetErrorString(e)));
   e = cudaDeviceSynchronize();
@@ -908,14 +927,17 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
 
 adi_status adi_layout(adi_patch P, int64_t* N, int64_t* k0, int64_t* k1) {
   CHECK_PATCH(P);
+  // balanced z-slabs: rank r owns planes [r N / R, (r+1) N / R)
+  const int64_t R = P->cfg.nranks, r = P->cfg.rank;
   if (N) *N = P->N;
-  if (k0) *k0 = 0;
-  if (k1) *k1 = P->N;
+  if (k0) *k0 = r * P->N / R;
+  if (k1) *k1 = (r + 1) * P->N / R;
   return ADI_OK;
 }
 
 adi_status adi_set_tau(adi_patch P, double tau) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (!(tau > 0.0) || !std::isfinite(tau)) return fail(ADI_ERR_ARG, "adi_set_tau: tau must be finite and > 0");
   const double old = P->tau;
   P->tau = tau;
@@ -949,6 +971,7 @@ static adi_status set_tf(adi_patch P, double* eps_new, double* mu_new) {
 
 adi_status adi_set_materials_tf(adi_patch P, const double* eps_tf, const double* mu_tf) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (!eps_tf) return fail(ADI_ERR_ARG, "adi_set_materials_tf: eps is NULL");
   double *e = nullptr, *m = nullptr;
   if (cudaMalloc(&e, P->U * sizeof(double)) != cudaSuccess || cudaMalloc(&m, P->U * sizeof(double)) != cudaSuccess) {
@@ -991,6 +1014,7 @@ static adi_status map_elements(adi_patch P, const double* d_elem, double* d_out,
 
 adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* mu_elem) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (!eps_elem) return fail(ADI_ERR_ARG, "adi_set_materials: eps is NULL");
   const int64_t ne = (int64_t)P->n * P->n * P->n;
   double *de = nullptr, *dw = nullptr, *e = nullptr, *m = nullptr;
@@ -1027,6 +1051,7 @@ adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* 
 
 adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (!f) return fail(ADI_ERR_ARG, "adi_set_fields: NULL array");
   for (int c = 0; c < 6; c++)
     if (!f[c]) return fail(ADI_ERR_ARG, "adi_set_fields: field %d is NULL", c);
@@ -1047,6 +1072,7 @@ adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
 
 adi_status adi_get_fields(adi_patch P, double* const f[6]) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (!f) return fail(ADI_ERR_ARG, "adi_get_fields: NULL array");
   for (int c = 0; c < 6; c++) {
     if (!f[c]) continue;
@@ -1060,6 +1086,7 @@ adi_status adi_get_fields(adi_patch P, double* const f[6]) {
 
 adi_status adi_set_source(adi_patch P, const double* const load[3], const double* signal, int64_t nsig) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (nsig < 0) return fail(ADI_ERR_ARG, "adi_set_source: nsig < 0");
   drop_graph(P);
   cudaStreamSynchronize(P->stream);
@@ -1126,6 +1153,7 @@ static adi_status run_steps(adi_patch P, int64_t k) {
 
 adi_status adi_step(adi_patch P, int64_t k) {
   CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
   if (k < 0) return fail(ADI_ERR_ARG, "adi_step: k < 0");
   if (!P->have_fields) return fail(ADI_ERR_STATE, "adi_step: fields not set");
   if (k == 0) return ADI_OK;
@@ -1312,6 +1340,149 @@ adi_status adi_debug_rhs_h(adi_patch P, int32_t s, const double* const Eo[3], co
   cudaError_t e = cudaStreamSynchronize(P->stream);
   if (!st && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "%s", cudaGetErrorString(e));
   for (int d = 0; d < 9; d++) cudaFree(t[d]);
+  return poison(P, st);
+}
+
+// ---- box-level entry points (slab-decomposed multi-GPU path) ---------------------
+static bool box_ok(const int64_t d[3]) { return d && d[0] > 0 && d[1] > 0 && d[2] > 0; }
+
+adi_status adi_box_sweep(adi_patch P, int32_t mode, int32_t njobs, const adi_sweep_job* jobs) {
+  CHECK_PATCH(P);
+  if (mode < 0 || mode > 2 || njobs < 1 || njobs > 3 || !jobs) return fail(ADI_ERR_ARG, "adi_box_sweep: bad args");
+  SweepReq r[3];
+  for (int j = 0; j < njobs; j++) {
+    const adi_sweep_job& J = jobs[j];
+    if (J.axis < 0 || J.axis > 2 || J.comp < 0 || J.comp > 5 || !box_ok(J.dims) || J.dims[J.axis] != P->N || !J.in ||
+        !J.out || (mode == 1 && (!J.c || !J.iu)) || (mode == 2 && !J.base))
+      return fail(ADI_ERR_ARG, "adi_box_sweep: bad job %d", j);
+    r[j] = SweepReq{J.comp, J.axis, J.in, J.out, J.iu, J.base, J.coef, {J.dims[0], J.dims[1], J.dims[2]}};
+  }
+  // the modified sweeps read c from the job (box layout), not from the patch
+  adi::SweepBatch B = make_batch(P, r, njobs);
+  for (int j = 0; j < njobs; j++) B.job[j].c = jobs[j].c;
+  B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
+  LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
+  const int64_t blocks_needed = ((int64_t)B.ntiles + adi::SW_WARPS - 1) / adi::SW_WARPS;
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[mode]);
+  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode); });
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_sweep: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+adi_status adi_box_factor(adi_patch P, int32_t comp, int32_t axis, const int64_t dims[3], const double* c, double* iu) {
+  CHECK_PATCH(P);
+  if (comp < 0 || comp > 5 || axis < 0 || axis > 2 || !box_ok(dims) || dims[axis] != P->N || !c || !iu)
+    return fail(ADI_ERR_ARG, "adi_box_factor: bad args");
+  SweepReq r{comp, axis, nullptr, nullptr, nullptr, nullptr, 0.0, {dims[0], dims[1], dims[2]}};
+  adi::SweepBatch B = make_batch(P, &r, 1);
+  B.job[0].c = c;
+  unsigned long long* bad;
+  if (cudaMallocAsync(&bad, sizeof *bad, P->stream) != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_factor: alloc"));
+  unsigned long long init = ~0ull, h = 0;
+  cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream);
+  const unsigned grid = (unsigned)std::min<int64_t>(((int64_t)B.ntiles * 32 + 127) / 128, (int64_t)P->nsm * 8);
+  with_degree(P->p, [&](auto ops) { ops.factor(P->stream, grid, B, iu, bad, 1e-14); });
+  cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, P->stream);
+  cudaFreeAsync(bad, P->stream);
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_factor: %s", cudaGetErrorString(e)));
+  if (h != ~0ull) return fail(ADI_ERR_SINGULAR, "adi_box_factor: tiny pivot (component %d, axis %d, fiber %llu)", comp, axis, h);
+  return ADI_OK;
+}
+
+adi_status adi_box_rhs(adi_patch P, int32_t kind, int32_t s, int32_t d, const double* const in[4], int64_t nzin,
+                       int64_t zoff, int64_t kg0, int64_t nzout, const double* a, const double* b, const double* c,
+                       const double* load, double sval, double* out) {
+  CHECK_PATCH(P);
+  const int nt = kind == 0 ? 4 : 3;
+  if ((kind != 0 && kind != 1) || (s != 1 && s != 2) || d < 0 || d > 2 || !in || !out || nzin < 1 || nzout < 1 ||
+      kg0 < 0 || kg0 + nzout > P->N || zoff < 0 || zoff + nzout > nzin || (kind == 0 && (!a || !c)) || (kind == 1 && !b))
+    return fail(ADI_ERR_ARG, "adi_box_rhs: bad args");
+  for (int t = 0; t < nt; t++)
+    if (!in[t]) return fail(ADI_ERR_ARG, "adi_box_rhs: input %d is NULL", t);
+  adi::RhsArgs args{};
+  for (int t = 0; t < nt; t++) args.u[t] = in[t];
+  args.nzin = (int)nzin;
+  args.zoff = (int)zoff;
+  args.kg0 = (int)kg0;
+  args.nzout = (int)nzout;
+  args.load = kind == 0 ? load : nullptr;
+  args.use_sdirect = 1;
+  args.sdirect = sval;
+  args.out = out;
+  // launch_rhs takes the row factors from the patch: point them at the caller's box arrays
+  double *pa = P->a, *pb = P->b, *pc = P->c;
+  P->a = const_cast<double*>(a), P->b = const_cast<double*>(b), P->c = const_cast<double*>(c);
+  adi_status st = launch_rhs(P, args, kind, s, kind == 0 ? d : 3 + d, kind == 0 ? ADI_K_RHS_E : ADI_K_RHS_H);
+  P->a = pa, P->b = pb, P->c = pc;
+  return poison(P, st);
+}
+
+adi_status adi_box_copy(adi_patch P, double* dst, const int64_t ddims[3], const int64_t doff[3], const double* src,
+                        const int64_t sdims[3], const int64_t soff[3], const int64_t ext[3]) {
+  CHECK_PATCH(P);
+  if (!dst || !src || !box_ok(ddims) || !box_ok(sdims) || !doff || !soff || !ext) return fail(ADI_ERR_ARG, "adi_box_copy: bad args");
+  for (int a = 0; a < 3; a++)
+    if (ext[a] < 0 || doff[a] < 0 || soff[a] < 0 || doff[a] + ext[a] > ddims[a] || soff[a] + ext[a] > sdims[a])
+      return fail(ADI_ERR_ARG, "adi_box_copy: box outside the arrays (axis %d)", a);
+  if (ext[0] * ext[1] * ext[2] == 0) return ADI_OK;
+  adi::copy_box_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(dst, ddims[0], ddims[1], doff[0], doff[1], doff[2], src, sdims[0],
+                                                          sdims[1], soff[0], soff[1], soff[2], ext[0], ext[1], ext[2]);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_copy: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+adi_status adi_box_abc(adi_patch P, const double* eps_tf, const double* mu_tf, int64_t count, double* a, double* b,
+                       double* c) {
+  CHECK_PATCH(P);
+  if (!eps_tf || !mu_tf || count < 0 || !a || !b || !c) return fail(ADI_ERR_ARG, "adi_box_abc: bad args");
+  adi::abc_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(eps_tf, mu_tf, P->tau, count, a, b, c);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_abc: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+adi_status adi_box_pec(adi_patch P, int32_t comp, double* u, const int64_t dims[3], const int64_t off[3]) {
+  CHECK_PATCH(P);
+  if (comp < 0 || comp > 5 || !u || !box_ok(dims) || !off) return fail(ADI_ERR_ARG, "adi_box_pec: bad args");
+  if (comp >= 3 || P->cfg.bc != ADI_BC_PEC) return ADI_OK;
+  int lo[3], hi[3];
+  for (int a = 0; a < 3; a++) active_range(P, comp, a, lo[a], hi[a]);
+  adi::pec_box_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(u, dims[0], dims[1], dims[2], off[0], off[1], off[2], lo[0], hi[0],
+                                                         lo[1], hi[1], lo[2], hi[2]);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_pec: %s", cudaGetErrorString(e)));
+  return ADI_OK;
+}
+
+adi_status adi_box_materials_tf(adi_patch P, const double* eps_elem, const double* mu_elem, double* eps_tf, double* mu_tf) {
+  CHECK_PATCH(P);
+  if (!eps_elem || !eps_tf || !mu_tf) return fail(ADI_ERR_ARG, "adi_box_materials_tf: bad args");
+  const int64_t ne = (int64_t)P->n * P->n * P->n;
+  double *de = nullptr, *dw = nullptr;
+  if (cudaMalloc(&de, ne * sizeof(double)) != cudaSuccess || cudaMalloc(&dw, P->wmat.size() * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(de);
+    return fail(ADI_ERR_OOM, "adi_box_materials_tf: cudaMalloc");
+  }
+  cudaMemcpy(dw, P->wmat.data(), P->wmat.size() * sizeof(double), cudaMemcpyHostToDevice);
+  adi_status st = copy_in(P, de, eps_elem, ne);
+  if (!st) st = check_positive(P, de, ne, "eps");
+  if (!st) st = map_elements(P, de, eps_tf, dw);
+  if (!st) {
+    if (mu_elem) {
+      st = copy_in(P, de, mu_elem, ne);
+      if (!st) st = check_positive(P, de, ne, "mu");
+      if (!st) st = map_elements(P, de, mu_tf, dw);
+    } else {
+      adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(mu_tf, P->U, 1.0);
+    }
+  }
+  cudaStreamSynchronize(P->stream);
+  cudaFree(de);
+  cudaFree(dw);
   return poison(P, st);
 }
 

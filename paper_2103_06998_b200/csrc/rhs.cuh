@@ -63,8 +63,12 @@ constexpr int RX_RING = 3;
 constexpr int RX_KCMAX = 64;  // max z-chunk (rows of the per-block z-coefficient table)
 
 struct RhsArgs {
-  int N;
+  int N;                      // global extent (x, y: the arrays' extents; z: of the patch)
   int kchunk;                 // z-planes per block
+  int nzin, zoff;             // input arrays hold nzin planes; output plane k <-> input plane k + zoff
+  int kg0, nzout;             // output arrays hold global planes [kg0, kg0 + nzout)
+  int use_sdirect;            // source amplitude given directly (sdirect) instead of signal[*step]
+  double sdirect;
   const double* tab;          // band tables, 4 ops
   const double* u[RX_MAXT];   // term inputs
   const double* a;            // tau/(2 eps^)
@@ -167,17 +171,19 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
     const bool yin = j0 >= 2 * P && j0 + RX_TY <= N - 2 * P;
     if (xin && yin) return;  // interior tile: the FAST launch owns it
   }
+  // output planes (local) [k0, k1); input planes (local) kin = k + zoff + q - P
   const int k0 = blockIdx.z * args.kchunk;
-  const int k1 = min(N, k0 + args.kchunk);
+  const int k1 = min(args.nzout, k0 + args.kchunk);
+  const int zoff = args.zoff, kg0 = args.kg0;
   const int i = i0 + tx;
   const int jA = j0 + 2 * ty;
   const int64_t NN = (int64_t)N * N;
-  const int kbeg = k0 - P, kend = k1 + P;  // input planes [kbeg, kend)
+  const int kbeg = k0 + zoff - P, kend = k1 + zoff + P;  // input planes [kbeg, kend)
 
   // per-block coefficient tables: rows of the band tables (0 outside [0,N))
   for (int e = tid; e < 3 * (k1 - k0) * W; e += RX_THREADS) {
     const int o = e / ((k1 - k0) * W), r = e - o * (k1 - k0) * W;
-    czs[o * RX_KCMAX * W + r] = args.tab[((int64_t)o * N + k0) * W + r];
+    czs[o * RX_KCMAX * W + r] = args.tab[((int64_t)o * N + kg0 + k0) * W + r];
   }
   if (!FAST) {
     for (int e = tid; e < 3 * RX_TX * W; e += RX_THREADS) {
@@ -210,7 +216,7 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
       }
     } else {
       if (kin < kend) {
-        const bool kok = kin >= 0 && kin < N;
+        const bool kok = kin >= 0 && kin < args.nzin;
         const int64_t pb = kok ? NN * kin : 0;
         for (int e = tid; e < PLANE; e += RX_THREADS) {
           const int yy = e / HX, xx = e - yy * HX;
@@ -236,9 +242,13 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
 #pragma unroll
       for (int q = 0; q < W; q++) w[t][r][q] = 0.0;
   double sval = 0.0;
-  if (KIND == 0 && args.load != nullptr && args.signal != nullptr) {
-    const int64_t s = *args.step;
-    if (s < args.nsig) sval = args.signal[s];
+  if (KIND == 0 && args.load != nullptr) {
+    if (args.use_sdirect) {
+      sval = args.sdirect;
+    } else if (args.signal != nullptr) {
+      const int64_t s = *args.step;
+      if (s < args.nsig) sval = args.signal[s];
+    }
   }
   const bool act_ij = i < N && i >= args.lo[0] && i < args.hi[0];
   const int u = tid & 15;  // x-pass: outputs 2u, 2u+1 of rows (tid >> 4) + 16 m
@@ -254,7 +264,7 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
         const double* slot = ring + st * NT * PLANEP;
         double* sxb = sx;
         // prefetch the row scales of the output plane k = kin - P
-        const int k = kin - P;
+        const int k = kin - P - zoff;  // output plane (local)
         const bool kout = k >= k0 && i < N;
         double sc[2][3];
 #pragma unroll
@@ -328,7 +338,7 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
         __syncthreads();  // sx consumed: the next plane's x-pass may overwrite it
         // ---- z-pass + row scaling for the output plane k = kin - P
         if (kout) {
-          const bool ak = act_ij && k >= args.lo[2] && k < args.hi[2];
+          const bool ak = act_ij && kg0 + k >= args.lo[2] && kg0 + k < args.hi[2];
           const double* zrow = czs + (k - k0) * W;
 #pragma unroll
           for (int r = 0; r < 2; r++) {

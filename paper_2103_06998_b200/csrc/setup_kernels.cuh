@@ -80,4 +80,25 @@ __global__ void minmax_pos_kernel(const double* __restrict__ x, int64_t n, unsig
   atomicMax(&mm[1], hi);
 }
 
+// dst box <- src box (3D strided copy; x fastest in both arrays)
+__global__ void copy_box_kernel(double* __restrict__ dst, int64_t dx, int64_t dy, int64_t ox, int64_t oy, int64_t oz,
+                                const double* __restrict__ src, int64_t sx, int64_t sy, int64_t px, int64_t py, int64_t pz,
+                                int64_t ex, int64_t ey, int64_t ez) {
+  const int64_t total = ex * ey * ez;
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < total; I += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = I % ex, y = (I / ex) % ey, z = I / (ex * ey);
+    dst[(ox + x) + dx * ((oy + y) + dy * (oz + z))] = src[(px + x) + sx * ((py + y) + sy * (pz + z))];
+  }
+}
+
+// zero the PEC-eliminated entries (D1) of an E component held in a box at global offset (ox, oy, oz)
+__global__ void pec_box_kernel(double* __restrict__ u, int64_t nx, int64_t ny, int64_t nz, int64_t ox, int64_t oy, int64_t oz,
+                               int lo0, int hi0, int lo1, int hi1, int lo2, int hi2) {
+  const int64_t total = nx * ny * nz;
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < total; I += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = ox + I % nx, j = oy + (I / nx) % ny, k = oz + I / (nx * ny);
+    if (i < lo0 || i >= hi0 || j < lo1 || j >= hi1 || k < lo2 || k >= hi2) u[I] = 0.0;
+  }
+}
+
 }  // namespace adi

@@ -37,9 +37,17 @@ constexpr int SW_MAXJOBS = 3;
 constexpr int SW_WARPS = 4;  // warps per block
 enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 // chunk rows (CH) and ring depth (RS) per mode
-constexpr int SW_CH_MASS = 16, SW_RS_MASS = 4;
-constexpr int SW_CH_MOD = 8, SW_RS_MOD = 5;
-constexpr int SW_CH_DER = 16, SW_RS_DER = 4;
+#ifndef ADI_SW_TUNE  // (tuning builds override these with -D)
+#define ADI_SW_CH_MASS 16
+#define ADI_SW_RS_MASS 4
+#define ADI_SW_CH_MOD 8
+#define ADI_SW_RS_MOD 5
+#define ADI_SW_CH_DER 16
+#define ADI_SW_RS_DER 4
+#endif
+constexpr int SW_CH_MASS = ADI_SW_CH_MASS, SW_RS_MASS = ADI_SW_RS_MASS;
+constexpr int SW_CH_MOD = ADI_SW_CH_MOD, SW_RS_MOD = ADI_SW_RS_MOD;
+constexpr int SW_CH_DER = ADI_SW_CH_DER, SW_RS_DER = ADI_SW_RS_DER;
 __host__ __device__ constexpr int sw_ch(int mode) { return mode == SW_MOD ? SW_CH_MOD : mode == SW_DER ? SW_CH_DER : SW_CH_MASS; }
 __host__ __device__ constexpr int sw_rs(int mode) { return mode == SW_MOD ? SW_RS_MOD : mode == SW_DER ? SW_RS_DER : SW_RS_MASS; }
 __host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? 3 : mode == SW_DER ? 2 : 1; }
@@ -62,13 +70,15 @@ struct SweepJob {
   int axis;           // 0 = x, 1 = y, 2 = z
   int lo, hi;         // active rows along the axis (PEC, D1)
   int var;            // band-table variant: 0 = [0,N), 1 = [1,N-1)
+  int dims[3];        // box extents (x fastest); dims[axis] = N (fibers span the patch)
+  int tile0;          // first tile of this job in the launch
 };
 
 struct SweepBatch {
   SweepJob job[SW_MAXJOBS];
   int njobs;
-  int N;
-  int ntiles;          // 32-fiber tiles per job = ceil(N^2 / 32)
+  int N;               // fiber length (global extent along the sweep axis)
+  int ntiles;          // 32-fiber tiles of all jobs
   int nck;             // checkpoint slots per warp (chunks per fiber)
   double* ckpt;        // per-warp checkpoint slots
   // constant (mass) factors per variant: rows = absolute row index, W entries:
@@ -108,19 +118,23 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_k
   const int gw = blockIdx.x * SW_WARPS + wib;
   const int nw = gridDim.x * SW_WARPS;
   const int N = B.N;
-  const int64_t NN = (int64_t)N * N;
   double* ck = B.ckpt + (size_t)gw * B.nck * SWD * 32 + lane;
-  const int total = B.njobs * B.ntiles;
+  const int total = B.ntiles;
 
   for (int t = gw; t < total; t += nw) {
-    const int jb = t / B.ntiles;
-    const int tile = t - jb * B.ntiles;
+    const int jb = (B.njobs > 1 && t >= B.job[1].tile0) + (B.njobs > 2 && t >= B.job[2].tile0);
     const double* src[3];
     double* out;
     double coef;
-    int axis, lo, hi, var;
+    int axis, lo, hi, var, nx, ny, tile;
+    int64_t NN;  // fibers of the job
     {
       const SweepJob& J = jb == 0 ? B.job[0] : jb == 1 ? B.job[1] : B.job[2];
+      tile = t - J.tile0;
+      nx = J.dims[0];
+      ny = J.dims[1];
+      NN = J.axis == 0 ? (int64_t)J.dims[1] * J.dims[2] : J.axis == 1 ? (int64_t)J.dims[0] * J.dims[2]
+                                                                       : (int64_t)J.dims[0] * J.dims[1];
       src[0] = J.in;
       src[1] = DER ? J.base : J.c;
       src[2] = J.iu;
@@ -138,12 +152,12 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_k
     int64_t base, stride;
     if (axis == 2) {
       base = fc;
-      stride = NN;
+      stride = (int64_t)nx * ny;
     } else if (axis == 1) {
-      base = (fc % N) + NN * (fc / N);
-      stride = N;
+      base = (fc % nx) + (int64_t)nx * ny * (fc / nx);
+      stride = nx;
     } else {
-      base = (int64_t)N * fc;
+      base = (int64_t)nx * fc;
       stride = 1;
     }
     const int nc = (hi - lo + CH - 1) / CH;
@@ -176,12 +190,12 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_k
         }
       } else {
         const int row = min(r0 + xr, hi - 1);
-        const int64_t o0 = (int64_t)N * f0 + row;
+        const int64_t o0 = (int64_t)nx * f0 + row;
         const int64_t fmax = NN - 1 - f0;  // last valid fiber offset in the tile
 #pragma unroll
         for (int m = 0; m < CH; m++) {
           const int ff = m * FPI + xf;
-          const int64_t off = ff <= fmax ? o0 + (int64_t)N * ff : o0;
+          const int64_t off = ff <= fmax ? o0 + (int64_t)nx * ff : o0;
           double* d = sl + xr * 33 + ff;
           sw_cp_async8(d, src[0] + off);
           if (NA > 1 && (!DER || na > 1)) sw_cp_async8(d + CH * 33, src[1] + off);
@@ -493,11 +507,11 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_k
         for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
         __syncwarp();
         const int row = r0 + xr;
-        double* po = out + (int64_t)N * f0 + row;
+        double* po = out + (int64_t)nx * f0 + row;
 #pragma unroll
         for (int m = 0; m < CH; m++) {
           const int ff = m * FPI + xf;
-          if (f0 + ff < NN && row < hi) po[(int64_t)N * ff] = sl[xr * 33 + ff];
+          if (f0 + ff < NN && row < hi) po[(int64_t)nx * ff] = sl[xr * 33 + ff];
         }
       }
       __syncwarp();
@@ -524,18 +538,19 @@ __global__ void factor_kernel(const SweepBatch B, double* __restrict__ iu_out, u
   constexpr int W = 2 * P + 1;
   const SweepJob& J = B.job[0];
   const int N = B.N;
-  const int64_t NN = (int64_t)N * N;
+  const int nx = J.dims[0], ny = J.dims[1];
+  const int64_t NN = J.axis == 0 ? (int64_t)J.dims[1] * J.dims[2] : J.axis == 1 ? (int64_t)nx * J.dims[2] : (int64_t)nx * ny;
   const int var = J.var;
   for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < NN; f += (int64_t)gridDim.x * blockDim.x) {
     int64_t base, stride;
     if (J.axis == 2) {
       base = f;
-      stride = NN;
+      stride = (int64_t)nx * ny;
     } else if (J.axis == 1) {
-      base = (f % N) + NN * (f / N);
-      stride = N;
+      base = (f % nx) + (int64_t)nx * ny * (f / nx);
+      stride = nx;
     } else {
-      base = (int64_t)N * f;
+      base = (int64_t)nx * f;
       stride = 1;
     }
     double uw[P][P], iw[P];

@@ -1,0 +1,143 @@
+"""CPU test double of the library's box-level kernels (adi_box_*), for the gloo
+tests of the slab-decomposed schedule (paper_2103_06998_b200.dist).
+
+Test infrastructure only: dense 1D matrices from the oracle, torch/numpy
+arithmetic on CPU tensors.  It restates the per-box operations from the paper
+(Kronecker terms of discrete1-discrete4 with the readings
+D1-D9, banded sweeps, the uniform-mu derivative projection) so that the
+orchestration -- which slab, which halo, which transpose, in which order -- can
+be checked against the oracle's single-domain step on CPU.
+"""
+import numpy as np
+import torch
+
+import oracle
+
+OP_M, OP_A, OP_B = 0, 1, 2
+
+
+def _v(t, dims):
+    """(z, y, x) numpy view of a flat/contiguous tensor holding a box of dims (x, y, z)."""
+    return t.numpy().reshape(int(dims[2]), int(dims[1]), int(dims[0]))
+
+
+class CpuBoxBackend:
+    def __init__(self, n, p, tau, bc=0):
+        self.O = oracle.Patch(n, p, tau, bc)
+        self.n, self.p, self.tau, self.bc = n, p, tau, bc
+        self.N = n + p
+        M, S, A = self.O.matrices()
+        self.M, self.S, self.A = M, S, A
+        self.ops = {OP_M: M, OP_A: A, OP_B: A.T.copy()}
+
+    def active(self, comp, axis):
+        if self.bc == 0 and comp < 3 and axis != comp:
+            return 1, self.N - 1
+        return 0, self.N
+
+    # -- data movement -------------------------------------------------------------
+    def box_copy(self, dst, ddims, doff, src, sdims, soff, ext):
+        d, s_ = _v(dst, ddims), _v(src, sdims)
+        d[doff[2]:doff[2] + ext[2], doff[1]:doff[1] + ext[1], doff[0]:doff[0] + ext[0]] = \
+            s_[soff[2]:soff[2] + ext[2], soff[1]:soff[1] + ext[1], soff[0]:soff[0] + ext[0]]
+
+    def box_abc(self, eps, mu, count, a, b, c):
+        e, m = eps.reshape(-1)[:count], mu.reshape(-1)[:count]
+        a.view(-1)[:count] = self.tau / (2.0 * e)
+        b.view(-1)[:count] = self.tau / (2.0 * m)
+        c.view(-1)[:count] = self.tau * self.tau / (4.0 * e * m)
+
+    def box_pec(self, comp, u, dims, off):
+        if comp >= 3 or self.bc != 0:
+            return
+        v = _v(u, dims)
+        for ax in range(3):
+            lo, hi = self.active(comp, ax)
+            idx = np.arange(dims[ax]) + off[ax]
+            bad = (idx < lo) | (idx >= hi)
+            sl = [slice(None)] * 3
+            sl[2 - ax] = bad
+            v[tuple(sl)] = 0.0
+
+    def box_materials_tf(self, eps_elem, mu_elem, eps_tf, mu_tf):
+        self.O.set_materials(np.asarray(eps_elem, dtype=np.float64), None if mu_elem is None else np.asarray(mu_elem))
+        e, m = self.O.get_materials_tf()
+        eps_tf.copy_(torch.from_numpy(e))
+        mu_tf.copy_(torch.from_numpy(m))
+
+    def box_factor(self, comp, axis, dims, c, iu):
+        pass  # the double solves each fiber directly
+
+    # -- sweeps -----------------------------------------------------------------------
+    def box_sweep(self, mode, jobs):
+        for j in jobs:
+            dims, ax = j["dims"], j["axis"]
+            lo, hi = self.active(j["comp"], ax)
+            u = np.moveaxis(_v(j["in"], dims), 2 - ax, -1).copy()  # fibers on the last axis
+            shp = u.shape
+            u = u.reshape(-1, shp[-1])
+            if mode == 0:
+                x = np.linalg.solve(self.M[lo:hi, lo:hi], u[:, lo:hi].T).T
+                res = u.copy()
+                res[:, lo:hi] = x
+            elif mode == 1:
+                cc = np.moveaxis(_v(j["c"], dims), 2 - ax, -1).reshape(-1, shp[-1])
+                res = u.copy()
+                for f in range(u.shape[0]):
+                    Af = self.M[lo:hi, lo:hi] + cc[f, lo:hi, None] * self.S[lo:hi, lo:hi]  # row scaling
+                    res[f, lo:hi] = np.linalg.solve(Af, u[f, lo:hi])
+            else:
+                base = np.moveaxis(_v(j["base"], dims), 2 - ax, -1).reshape(-1, shp[-1])
+                res = base + j["coef"] * np.linalg.solve(self.M, self.A @ u.T).T
+            out = _v(j["out"], dims)
+            out[...] = np.moveaxis(res.reshape(shp), -1, 2 - ax)
+
+    # -- right-hand sides -------------------------------------------------------------
+    def _program(self, kind, s, d):
+        """[(input index, ops per axis (x, y, z), scale name, sign)] of SURVEY §8(a) a1/a3/a5/a7."""
+        sig = (d + 1) % 3 if s == 1 else (d + 2) % 3
+        def ops(**kw):
+            o = [OP_M, OP_M, OP_M]
+            for ax, op in kw.items():
+                o[int(ax[1])] = op
+            return o
+        if kind == 0:
+            t3 = [OP_M, OP_M, OP_M]
+            t3[d] = OP_A
+            t3[sig] = OP_B
+            return [(0, [OP_M] * 3, "one", 1.0), (1, ops(**{f"a{(d + 1) % 3}": OP_A}), "a", 1.0),
+                    (2, ops(**{f"a{(d + 2) % 3}": OP_A}), "a", -1.0), (3, t3, "c", 1.0)]
+        if s == 1:
+            return [(0, [OP_M] * 3, "one", 1.0), (1, ops(**{f"a{(d + 1) % 3}": OP_A}), "b", -1.0),
+                    (2, ops(**{f"a{(d + 2) % 3}": OP_A}), "b", 1.0)]
+        return [(0, [OP_M] * 3, "one", 1.0), (1, ops(**{f"a{(d + 2) % 3}": OP_A}), "b", 1.0),
+                (2, ops(**{f"a{(d + 1) % 3}": OP_A}), "b", -1.0)]
+
+    def box_rhs(self, kind, s, d, ins, nzin, zoff, kg0, nzout, a, b, c, load, sval, out):
+        N = self.N
+        zwin = np.arange(nzin) + kg0 - zoff  # global planes held by the inputs
+        ok = (zwin >= 0) & (zwin < N)
+        acc = {"one": 0.0, "a": 0.0, "b": 0.0, "c": 0.0}
+        for t, opx, sc, sign in self._program(kind, s, d):
+            u = ins[t].numpy().reshape(nzin, N, N)
+            X, Y, Z = self.ops[opx[0]], self.ops[opx[1]], self.ops[opx[2]]
+            Zr = np.zeros((nzout, nzin))
+            Zr[:, ok] = Z[kg0:kg0 + nzout][:, zwin[ok]]
+            v = np.einsum("kz,zyx->kyx", Zr, u)
+            v = np.einsum("jy,kyx->kjx", Y, v)
+            v = np.einsum("ix,kjx->kji", X, v)
+            acc[sc] = acc[sc] + sign * v
+        sh = (nzout, N, N)
+        res = acc["one"]
+        if kind == 0:
+            av, cv = a.numpy().reshape(sh), c.numpy().reshape(sh)
+            res = res + av * acc["a"] + cv * acc["c"]
+            if load is not None and sval != 0.0:
+                res = res - av * sval * load.numpy().reshape(sh)
+            comp = d
+        else:
+            res = res + b.numpy().reshape(sh) * acc["b"]
+            comp = 3 + d
+        o = out.numpy().reshape(sh)
+        o[...] = res
+        self.box_pec(comp, out, (N, N, nzout), (0, 0, kg0))

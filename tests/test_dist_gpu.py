@@ -1,0 +1,135 @@
+"""Slab-decomposed path on one B200 with the CUDA box kernels (adi_box_*).
+
+R = 1 through DistPatch (halo'd slab RHS, z-sweeps on the y-slab layout) and
+R = 2 / 3 as threads of one process sharing cuda:0: each thread owns a box-mode
+library patch (rank r of R) and its slab buffers; the exchanges go through an
+in-process stand-in of torch.distributed (ThreadComm: device copies between the
+threads' tensors after a host barrier -- no kernel ever waits on another
+rank's kernel).  Results must match the oracle to 1e-10 and the R = 1 run bit for
+bit (per-fiber arithmetic is independent of the decomposition).
+"""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from paper_2103_06998_b200.dist import DistPatch, SlabPlan
+
+pytestmark = pytest.mark.gpu
+
+
+class ThreadComm:
+    """halo_exchange / z2y / y2z of rank `rank` among threads sharing `shared`."""
+
+    def __init__(self, plan: SlabPlan, rank: int, shared):
+        self.plan, self.rank, self.sh = plan, rank, shared
+
+    def _post(self, obj):
+        torch.cuda.synchronize()
+        self.sh["post"][self.rank] = obj
+        self.sh["bar"].wait()
+
+    def _done(self):
+        torch.cuda.synchronize()
+        self.sh["bar"].wait()
+
+    def halo_exchange(self, fields):
+        pl, r, P = self.plan, self.rank, self.plan.p
+        nz = pl.nz(r)
+        self._post(fields)
+        if r > 0:
+            nb = self.sh["post"][r - 1]
+            nzb = pl.nz(r - 1)
+            for f, g in zip(fields, nb):
+                f[0:P].copy_(g[nzb:nzb + P])
+        if r < pl.R - 1:
+            nb = self.sh["post"][r + 1]
+            for f, g in zip(fields, nb):
+                f[nz + P:nz + 2 * P].copy_(g[P:2 * P])
+        self._done()
+
+    def z2y(self, src, dst, sendbuf):
+        pl, r = self.plan, self.rank
+        j0, j1 = pl.j[r]
+        self._post(src)
+        for q in range(pl.R):
+            k0, k1 = pl.k[q]
+            dst[k0:k1].copy_(self.sh["post"][q][:, j0:j1, :])
+        self._done()
+
+    def y2z(self, src, dst, recvbuf):
+        pl, r = self.plan, self.rank
+        k0, k1 = pl.k[r]
+        self._post(src)
+        for q in range(pl.R):
+            j0, j1 = pl.j[q]
+            dst[:, j0:j1, :].copy_(self.sh["post"][q][k0:k1])
+        self._done()
+
+
+def run_ranks(R, n, p, tau, steps, mu_kind="uniform", source=False):
+    N = n + p
+    shared = {"bar": threading.Barrier(R), "post": [None] * R}
+    out = [None] * R
+    err = []
+    eps = workloads.element_eps(n, "phantom4" if n >= 8 else "random", seed=4)
+    mu = None if mu_kind == "uniform" else workloads.element_eps(n, "random", seed=6) / 40.0
+    f = [x.reshape(N, N, N) for x in workloads.random_fields(N, 17)]
+
+    def work(r):
+        try:
+            torch.cuda.set_device(0)
+            plan = SlabPlan(N, p, R)
+            D = DistPatch(n, p, tau, rank=r, nranks=R, comm=ThreadComm(plan, r, shared) if R > 1 else None)
+            D.set_materials(eps, mu)
+            D.set_fields([torch.from_numpy(np.ascontiguousarray(x[D.k0:D.k1])) for x in f])
+            if source:
+                O = oracle.Patch(n, p, tau)
+                D.set_source([None, None, O.point_load(*workloads.dipole_position(n))],
+                             workloads.signal("modsine", tau, steps))
+            D.step(steps)
+            torch.cuda.synchronize()
+            out[r] = np.stack([x.cpu().numpy() for x in D.get_fields()])
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+            shared["bar"].abort()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if err:
+        raise err[0]
+    return np.concatenate(out, axis=1), eps, mu, f
+
+
+def oracle_ref(n, p, tau, steps, eps, mu, f, source=False):
+    O = oracle.Patch(n, p, tau)
+    O.set_materials(eps, mu)
+    O.set_fields([x.reshape(-1) for x in f])
+    if source:
+        O.set_source([None, None, O.point_load(*workloads.dipole_position(n))], workloads.signal("modsine", tau, steps))
+    O.step(steps)
+    return [x.reshape(n + p, n + p, n + p) for x in O.get_fields()]
+
+
+@pytest.mark.parametrize("R,n,p,mu_kind,source", [(1, 10, 2, "uniform", False), (2, 10, 2, "uniform", True),
+                                                  (3, 9, 3, "uniform", False), (2, 8, 2, "random", False)])
+def test_dist_threads_match_oracle(R, n, p, mu_kind, source):
+    tau, steps = 0.02, 2
+    got, eps, mu, f = run_ranks(R, n, p, tau, steps, mu_kind, source)
+    ref = oracle_ref(n, p, tau, steps, eps, mu, f, source)
+    for c in range(6):
+        e = np.linalg.norm(got[c] - ref[c]) / np.linalg.norm(ref[c])
+        assert e <= 1e-10, (c, e)
+
+
+def test_dist_decomposition_invariance_bitwise():
+    """R = 1, 2, 4 slab decompositions give bit-identical fields."""
+    outs = [run_ranks(R, 14, 2, 0.01, 2)[0] for R in (1, 2, 4)]
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
