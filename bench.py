@@ -214,7 +214,7 @@ def run_reference(args, cfg):
     out = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(cfg, args),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -229,9 +229,91 @@ def config_dict(cfg, args):
                      f"material={cfg['material']}, seeded random fields"),
         "n": n, "p": p, "N": n + p, "tau": cfg["tau"], "dof_per_step": dof_count(n, p),
         "l2_policy": "inputs larger than L2 (each field %.2f GB > 126 MB)" % ((n + p) ** 3 * 8 / 1e9),
-        "parallelism": ("single GPU" if args.gpus == 1 else
-                        f"{args.gpus} independent replicas (slab decomposition not yet implemented)"),
+        "parallelism": ("single GPU, whole patch, CUDA graph per step" if args.gpus == 1 else
+                        f"z-slab decomposition over {args.gpus} GPUs: NCCL halo exchange before the RHS, "
+                        "all-to-all z<->y transposes around z-sweeps (paper_2103_06998_b200.dist)"),
     }
+
+
+class _Whole:
+    """Single GPU: the whole patch in one library handle, one CUDA graph per step."""
+
+    def __init__(self, cfg, local, seed):
+        import paper_2103_06998_b200 as adi
+
+        n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
+        self.N = n + p
+        eps, self.fields = make_inputs(cfg, seed=seed, pinned=True)
+        self.G = adi.Patch(n, p, tau, device=local)
+        self.G.set_materials(eps)
+        self.G.set_fields(self.fields)
+        self.stream_handle = self.G.stream
+        self.local_bytes = 6 * self.N ** 3 * 8
+
+    def step(self, k):
+        self.G.step(k)
+
+    def timing(self, on):
+        self.G.set_timing(on)
+
+    def report(self):
+        return self.G.timing_report()
+
+    def e2e(self, out_host):
+        self.G.set_fields(self.fields)  # pinned host -> device
+        self.G.step(self.k_e2e)
+        self.G.get_fields(out_host)     # device -> pinned host (synchronises)
+
+    def launches_per_step(self):
+        return self.G.launches_per_step
+
+    def close(self):
+        self.G.close()
+
+
+class _Slabs:
+    """N > 1 GPUs: this rank's z-slab (paper_2103_06998_b200.dist), exchanges over NCCL."""
+
+    def __init__(self, cfg, local, seed):
+        import torch
+
+        from paper_2103_06998_b200.dist import DistPatch
+
+        n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
+        self.N = N = n + p
+        self.D = DistPatch(n, p, tau, device=local)
+        self.D.set_materials(workloads.element_eps(n, cfg["material"]))
+        rng = np.random.default_rng(seed)
+        nz = self.D.nz
+        self.fields = [torch.from_numpy(rng.uniform(-1.0, 1.0, size=(nz, N, N))).pin_memory() for _ in range(6)]
+        self.D.set_fields(self.fields)
+        self.stream_handle = torch.cuda.current_stream(local).cuda_stream
+        self.local_bytes = 6 * nz * N * N * 8
+
+    def step(self, k):
+        self.D.step(k)
+
+    def timing(self, on):
+        self.D.B.set_timing(on)
+
+    def report(self):
+        return self.D.B.timing_report()
+
+    def e2e(self, out_host):
+        self.D.set_fields(self.fields)
+        self.D.step(self.k_e2e)
+        for o, f in zip(out_host, self.D.get_fields()):
+            o.copy_(f.view(-1))
+
+    def launches_per_step(self):
+        self.D.B.set_timing(True)
+        self.D.step(1)
+        rep = self.D.B.timing_report()
+        self.D.B.set_timing(False)
+        return sum(v[1] for v in rep.values())
+
+    def close(self):
+        pass
 
 
 def run_ours(args, cfg):
@@ -246,15 +328,11 @@ def run_ours(args, cfg):
     n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
     N = n + p
     U = N ** 3
-    eps, fields = make_inputs(cfg, seed=1000 + rank, pinned=True)
-    G = adi.Patch(n, p, tau, device=local)
-    G.set_materials(eps)
-    del eps
-    G.set_fields(fields)
-    G.step(args.warmup)
-    G.synchronize()
-    # ---------------- timed region (device-resident state, CUDA graph per step) ----
-    stream = torch.cuda.ExternalStream(G.stream, device=local)
+    S = (_Whole if ws == 1 else _Slabs)(cfg, local, 1000 + rank)
+    S.step(args.warmup)
+    torch.cuda.synchronize()
+    # ---------------- timed region (device-resident state) ----------------
+    stream = torch.cuda.ExternalStream(S.stream_handle, device=local)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     if dist:
@@ -262,7 +340,7 @@ def run_ours(args, cfg):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record(stream)
-        G.step(args.steps)
+        S.step(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
     if dist:
@@ -270,33 +348,34 @@ def run_ours(args, cfg):
     ms = e0.elapsed_time(e1)
     clocks = clk.summary()
     # ---------------- per-kernel breakdown (same steps, each launch bracketed by events) ----
-    G.set_timing(True)
-    G.step(max(1, min(args.steps, 3)))
-    rep = G.timing_report()
-    G.set_timing(False)
+    S.timing(True)
+    S.step(max(1, min(args.steps, 3)))
+    rep = S.report()
+    S.timing(False)
+    lps = S.launches_per_step()
     # ---------------- end-to-end through the public API, host buffers ---------
-    out_host = [torch.empty(U, dtype=torch.float64, pin_memory=True) for _ in range(6)]
+    out_host = [torch.empty(S.local_bytes // 48, dtype=torch.float64, pin_memory=True) for _ in range(6)]
+    S.k_e2e = args.steps
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
-    G.set_fields(fields)  # pinned host -> device (synchronous)
-    G.step(args.steps)    # graph path
-    G.get_fields(out_host)  # device -> pinned host (synchronises)
+    S.e2e(out_host)
+    torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    h2d = 6 * U * 8 / args.steps
-    d2h = 6 * U * 8 / args.steps
-    launches = args.steps * G.launches_per_step  # kernels of this library in the timed region
+    h2d = S.local_bytes * ws / args.steps
+    d2h = S.local_bytes * ws / args.steps
+    launches = args.steps * lps  # kernels of this library in the timed region (per rank)
     ms_t = torch.tensor([ms, e2e_s * 1e3], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms, e2e_ms = float(ms_t[0]), float(ms_t[1])
     if rank != 0:
-        G.close()
+        S.close()
         return
     dofs = dof_count(n, p)
-    value = ws * dofs * args.steps / (ms * 1e-3)
-    e2e_value = ws * dofs * args.steps / (e2e_ms * 1e-3)
+    value = dofs * args.steps / (ms * 1e-3)  # the whole patch (all ranks together)
+    e2e_value = dofs * args.steps / (e2e_ms * 1e-3)
     # roofline of the dominant kernel class
     peak, peak_src = hbm_peak()
     algo = algorithmic_bytes(n, p)
@@ -328,7 +407,7 @@ def run_ours(args, cfg):
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, args),
         "roofline": {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -343,7 +422,7 @@ def run_ours(args, cfg):
         "clocks": clocks,
     }
     print(json.dumps(out), flush=True)
-    G.close()
+    S.close()
 
 
 def main():

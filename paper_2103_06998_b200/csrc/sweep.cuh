@@ -45,6 +45,9 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #define ADI_SW_CH_DER 16
 #define ADI_SW_RS_DER 4
 #endif
+#ifndef ADI_SW_MINB_MASS  // resident blocks the mass kernel's register budget is sized for
+#define ADI_SW_MINB_MASS 2
+#endif
 constexpr int SW_CH_MASS = ADI_SW_CH_MASS, SW_RS_MASS = ADI_SW_RS_MASS;
 constexpr int SW_CH_MOD = ADI_SW_CH_MOD, SW_RS_MOD = ADI_SW_RS_MOD;
 constexpr int SW_CH_DER = ADI_SW_CH_DER, SW_RS_DER = ADI_SW_RS_DER;
@@ -104,7 +107,7 @@ template <int N>
 __device__ __forceinline__ void sw_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MOD ? 1 : 3) sweep_kernel(const __grid_constant__ SweepBatch B) {
+__global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_MASS : 1) sweep_kernel(const __grid_constant__ SweepBatch B) {
   constexpr bool MOD = MODE == SW_MOD, DER = MODE == SW_DER;
   constexpr int CH = sw_ch(MODE), RS = sw_rs(MODE), NA = sw_na(MODE);
   constexpr int W = 2 * P + 1;

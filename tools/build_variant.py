@@ -10,7 +10,7 @@ sys.path.insert(0, ROOT)
 import paper_2103_06998_b200 as adi  # noqa: E402
 
 name, *v = sys.argv[1:]
-keys = ["CH_MASS", "RS_MASS", "CH_MOD", "RS_MOD", "CH_DER", "RS_DER"]
+keys = ["CH_MASS", "RS_MASS", "CH_MOD", "RS_MOD", "CH_DER", "RS_DER", "MINB_MASS"]
 flags = ["-DADI_SW_TUNE"] + [f"-DADI_SW_{k}={x}" for k, x in zip(keys, v)]
 path = os.path.join(ROOT, "build", "variants", name, "libadimaxwell.so")
 print(adi.build(force=True, lib_path=path, extra_flags=flags))
