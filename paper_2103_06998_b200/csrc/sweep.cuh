@@ -42,7 +42,7 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #define ADI_SW_RS_MASS 4
 #define ADI_SW_CH_MOD 8
 #define ADI_SW_RS_MOD 5
-#define ADI_SW_CH_DER 16
+#define ADI_SW_CH_DER 8
 #define ADI_SW_RS_DER 4
 #endif
 #ifndef ADI_SW_MINB_MASS  // resident blocks the mass kernel's register budget is sized for
