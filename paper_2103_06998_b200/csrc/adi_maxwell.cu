@@ -173,6 +173,13 @@ struct adi_patch_s {
   size_t ckpt_words = 0;
   double* iu[6] = {};       // cached pivots 1/u_kk of the six row-modified families (s, d)
   int hk[2] = {0, 0}, tk[2] = {0, 0};  // mass factor rows equal to the interior row
+  bool tw_ok[2] = {false, false};      // twisted (two-segment SPIKE) tables built for the variant
+  double* d_sp[2] = {nullptr, nullptr};
+  int tw_m1[2] = {0, 0};
+  int tw_spl[2] = {0, 0}, tw_sph[2] = {0, 0};
+  double tw_vb[2][25] = {}, tw_wt[2][25] = {}, tw_kk[2][25] = {};
+  int sw_grid_tw[3] = {0, 0, 0};       // persistent grid of the twisted mass / - / derivative sweep
+  int use_tw = 0;                      // ADI_SW_TWISTED=1 enables the twisted (two-segment SPIKE) sweeps
   std::vector<double> kfac[2];
   std::vector<double> kM, kS;          // interior Toeplitz rows of M, S
   int sw_grid[3] = {0, 0, 0};          // persistent grid of the mass / modified / derivative sweep
@@ -393,7 +400,7 @@ struct SweepReq {
   int64_t dims[3] = {0, 0, 0};   // box extents (x fastest); 0 = the whole N^3 patch
 };
 
-adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
+adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_fibers = 32) {
   adi::SweepBatch B{};
   B.N = P->N;
   B.njobs = nreq;
@@ -405,7 +412,7 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
     const int ax = req[j].axis;
     const int64_t nfib = (int64_t)J.dims[(ax + 1) % 3] * J.dims[(ax + 2) % 3];
     J.tile0 = (int)tiles;
-    tiles += (nfib + 31) / 32;
+    tiles += (nfib + tile_fibers - 1) / tile_fibers;
     J.in = req[j].in;
     J.out = req[j].out;
     J.c = P->c;
@@ -427,33 +434,53 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq) {
   }
   for (int q = 0; q < P->W; q++) B.kM[q] = P->kM[q], B.kS[q] = P->kS[q];
   B.Ab = P->d_tab + (size_t)adi::OP_A * P->N * P->W;
+  for (int v = 0; v < 2; v++) {
+    B.sp[v] = P->d_sp[v];
+    B.m1[v] = P->tw_m1[v];
+    B.spl[v] = P->tw_spl[v];
+    B.sph[v] = P->tw_sph[v];
+    for (int i = 0; i < 25; i++) B.vb[v][i] = P->tw_vb[v][i], B.wt[v][i] = P->tw_wt[v][i], B.kk[v][i] = P->tw_kk[v][i];
+  }
   for (int q = 0; q < P->W; q++) B.kA[q] = P->tab_host[((size_t)adi::OP_A * P->N + P->N / 2) * P->W + q];
   return B;
 }
 
+// twisted (two-segment SPIKE) launch possible for these jobs?
+bool twisted(adi_patch P, const SweepReq* req, int nreq, int mode) {
+  if (!P->use_tw || mode == adi::SW_MOD) return false;
+  for (int j = 0; j < nreq; j++) {
+    int lo, hi;
+    active_range(P, req[j].comp, req[j].axis, lo, hi);
+    if (!P->tw_ok[lo == 0 ? 0 : 1]) return false;
+  }
+  return true;
+}
+
 adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode) {
-  adi::SweepBatch B = make_batch(P, req, nreq);
+  const bool tw = twisted(P, req, nreq, mode);
+  adi::SweepBatch B = make_batch(P, req, nreq, tw ? 16 : 32);
   B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
   LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
   const int64_t warps_needed = B.ntiles;
   const int64_t blocks_needed = (warps_needed + adi::SW_WARPS - 1) / adi::SW_WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[mode]);
-  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode); });
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, tw ? P->sw_grid_tw[mode] : P->sw_grid[mode]);
+  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode, tw); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
 
 adi_status sweep_setup(adi_patch P) {
-  int occ[3] = {0, 0, 0};
-  cudaError_t e = with_degree(P->p, [&](auto ops) { return ops.sweep_attrs(occ); });
-  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1 || occ[2] < 1) {
+  int occ[3] = {0, 0, 0}, occ_tw[3] = {0, 0, 0};
+  cudaError_t e = with_degree(P->p, [&](auto ops) { return ops.sweep_attrs(occ, occ_tw); });
+  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1 || occ[2] < 1 || occ_tw[0] < 1 || occ_tw[2] < 1) {
     cudaGetLastError();
     return fail(ADI_ERR_CUDA, "sweep kernel attributes: %s", cudaGetErrorString(e));
   }
   for (int m = 0; m < 3; m++) {
-    int bps = occ[m];
-    if (P->sw_bps[m] > 0) bps = std::min(bps, P->sw_bps[m]);
+    int bps = occ[m], bps_tw = occ_tw[m];
+    if (P->sw_bps[m] > 0) bps = std::min(bps, P->sw_bps[m]), bps_tw = std::min(bps_tw, P->sw_bps[m]);
     P->sw_grid[m] = P->nsm * bps;
+    P->sw_grid_tw[m] = P->nsm * bps_tw;
   }
   return ADI_OK;
 }
@@ -618,6 +645,82 @@ bool mass_factor(const std::vector<double>& M, int N, int p, int lo, int hi, std
   return true;
 }
 
+// Dense solve of A X = B (n x n SPD, no pivoting; n <= N), B overwritten with X (n x m, row-major)
+void dense_solve(std::vector<double> A, int n, std::vector<double>& Bm, int m) {
+  for (int k = 0; k < n; k++) {
+    const double piv = A[(size_t)k * n + k];
+    for (int i = k + 1; i < n; i++) {
+      const double l = A[(size_t)i * n + k] / piv;
+      if (l == 0.0) continue;
+      for (int j = k; j < n; j++) A[(size_t)i * n + j] -= l * A[(size_t)k * n + j];
+      for (int j = 0; j < m; j++) Bm[(size_t)i * m + j] -= l * Bm[(size_t)k * m + j];
+    }
+  }
+  for (int i = n - 1; i >= 0; i--) {
+    for (int j = 0; j < m; j++) {
+      double x = Bm[(size_t)i * m + j];
+      for (int k = i + 1; k < n; k++) x -= A[(size_t)i * n + k] * Bm[(size_t)k * m + j];
+      Bm[(size_t)i * m + j] = x / A[(size_t)i * n + i];
+    }
+  }
+}
+
+// Two-segment SPIKE tables of the mass matrix restricted to [lo, hi) (sweep_tw.cuh):
+// split m1 = lo + ceil(L/2); V1 = A1^{-1} B (B: columns m1..m1+p-1 of the top rows),
+// W2 = A2^{-1} C (C: columns m1-p..m1-1 of the bottom rows); interface matrices
+// Vb = V1[m1-p..m1-1], Wt = W2[m1..m1+p-1], K = (I - Vb Wt)^{-1}.
+bool spike_tables(const std::vector<double>& M, int N, int p, int lo, int hi, std::vector<double>& sp, int& m1,
+                  double* vb, double* wt, double* kk, int& spl, int& sph) {
+  const int L = hi - lo;
+  if (L < 4 * p + 2) return false;
+  const int n1 = (L + 1) / 2, n2 = L - n1;
+  m1 = lo + n1;
+  auto Mat = [&](int i, int j) { return M[(size_t)(lo + i) * N + (lo + j)]; };
+  std::vector<double> A1((size_t)n1 * n1), A2((size_t)n2 * n2), V((size_t)n1 * p, 0.0), Wm((size_t)n2 * p, 0.0);
+  for (int i = 0; i < n1; i++)
+    for (int j = 0; j < n1; j++) A1[(size_t)i * n1 + j] = Mat(i, j);
+  for (int i = 0; i < n2; i++)
+    for (int j = 0; j < n2; j++) A2[(size_t)i * n2 + j] = Mat(n1 + i, n1 + j);
+  for (int i = 0; i < n1; i++)
+    for (int j = 0; j < p; j++) V[(size_t)i * p + j] = Mat(i, n1 + j);
+  for (int i = 0; i < n2; i++)
+    for (int j = 0; j < p; j++) Wm[(size_t)i * p + j] = Mat(n1 + i, n1 - p + j);
+  dense_solve(A1, n1, V, p);
+  dense_solve(A2, n2, Wm, p);
+  sp.assign((size_t)N * p, 0.0);
+  for (int i = 0; i < n1; i++)
+    for (int j = 0; j < p; j++) sp[(size_t)(lo + i) * p + j] = V[(size_t)i * p + j];
+  for (int i = 0; i < n2; i++)
+    for (int j = 0; j < p; j++) sp[(size_t)(m1 + i) * p + j] = Wm[(size_t)i * p + j];
+  std::vector<double> Iv((size_t)p * p, 0.0), Kk((size_t)p * p, 0.0);
+  for (int a = 0; a < p; a++)
+    for (int b = 0; b < p; b++) {
+      vb[a * p + b] = V[(size_t)(n1 - p + a) * p + b];
+      wt[a * p + b] = Wm[(size_t)a * p + b];
+    }
+  for (int a = 0; a < p; a++)
+    for (int b = 0; b < p; b++) {
+      double s = a == b ? 1.0 : 0.0;
+      for (int c = 0; c < p; c++) s -= vb[a * p + c] * wt[c * p + b];
+      Iv[(size_t)a * p + b] = s;
+      Kk[(size_t)a * p + b] = a == b ? 1.0 : 0.0;
+    }
+  dense_solve(Iv, p, Kk, p);
+  for (int i = 0; i < p * p; i++) kk[i] = Kk[i];
+  // rows whose spike entries are all below 1e-20 of the largest are dropped from the correction
+  double vmax = 0.0;
+  for (double v : sp) vmax = std::max(vmax, std::fabs(v));
+  spl = m1;
+  sph = m1;
+  for (int r = lo; r < hi; r++)
+    for (int j = 0; j < p; j++)
+      if (std::fabs(sp[(size_t)r * p + j]) > 1e-20 * vmax) {
+        spl = std::min(spl, r);
+        sph = std::max(sph, r + 1);
+      }
+  return true;
+}
+
 bool is_device_ptr(const void* ptr) {
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -725,7 +828,7 @@ void adi_destroy(adi_patch P) {
   drop_graph(P);
   auto f = [](void* x) { if (x) cudaFree(x); };
   f(P->d_tab);
-  for (int v = 0; v < 2; v++) f(P->d_fac[v]), f(P->d_Mb[v]), f(P->d_Sb[v]);
+  for (int v = 0; v < 2; v++) f(P->d_fac[v]), f(P->d_Mb[v]), f(P->d_Sb[v]), f(P->d_sp[v]);
   for (int i = 0; i < 6; i++) f(P->F[i]);
   for (int i = 0; i < 3; i++) f(P->R[i]), f(P->G[i]), f(P->load[i]);
   f(P->a), f(P->b), f(P->c), f(P->epsh), f(P->muh), f(P->ckpt), f(P->signal), f(P->d_step);
@@ -775,6 +878,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_SW_BPS_MOD")) P->sw_bps[1] = atoi(s);
   if (const char* s = getenv("ADI_SW_BPS_DER")) P->sw_bps[2] = atoi(s);
   if (const char* s = getenv("ADI_H_GENERAL")) P->h_general = atoi(s);
+  if (const char* s = getenv("ADI_SW_TWISTED")) P->use_tw = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   {
@@ -792,9 +896,32 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   // bank (a rounding-level change of the matrices).
   if (N > 4 * p) {
     const int mid = N / 2;
+    // the interior stencil is symmetric (M, S) / antisymmetric (A); make the copied row exactly so
+    for (int q = 1; q <= p; q++) {
+      const size_t r = (size_t)mid * N + mid;
+      P->M[r - q] = P->M[r + q];
+      P->S[r - q] = P->S[r + q];
+      P->A[r - q] = -P->A[r + q];
+    }
+    P->A[(size_t)mid * N + mid] = 0.0;
     for (std::vector<double>* X : {&P->M, &P->S, &P->A})
       for (int r = 2 * p; r < N - 2 * p; r++)
         for (int q = -p; q <= p; q++) (*X)[(size_t)r * N + r + q] = (*X)[(size_t)mid * N + mid + q];
+  }
+  // The basis is symmetric under x -> 1 - x (B_i(1-x) = B_{N-1-i}(x)), so M and S are
+  // persymmetric and A anti-persymmetric: X[N-1-i][N-1-j] = +-X[i][j].  Mirror the top
+  // rows onto the bottom ones (again a rounding-level change) so that the twisted
+  // sweeps can solve the bottom half-fiber with the top half's LU factors.
+  for (int i = 0; i < N; i++) {
+    const int ii = N - 1 - i;
+    if (ii <= i) break;
+    for (int q = -p; q <= p; q++) {
+      const int j = i + q, jj = N - 1 - j;
+      if (j < 0 || j >= N) continue;
+      P->M[(size_t)ii * N + jj] = P->M[(size_t)i * N + j];
+      P->S[(size_t)ii * N + jj] = P->S[(size_t)i * N + j];
+      P->A[(size_t)ii * N + jj] = -P->A[(size_t)i * N + j];
+    }
   }
   // material weights (D6): w[r*n+e] = int_{elem e} B_r / int B_r (Gauss q = p+1, exact)
   {
@@ -870,6 +997,13 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     cudaMemcpy(P->d_fac[var], fac.data(), fac.size() * sizeof(double), cudaMemcpyHostToDevice);
     cudaMemcpy(P->d_Mb[var], Mb.data(), Mb.size() * sizeof(double), cudaMemcpyHostToDevice);
     cudaMemcpy(P->d_Sb[var], Sb.data(), Sb.size() * sizeof(double), cudaMemcpyHostToDevice);
+    std::vector<double> sp;
+    P->tw_ok[var] = spike_tables(P->M, N, p, lo, hi, sp, P->tw_m1[var], P->tw_vb[var], P->tw_wt[var], P->tw_kk[var],
+                                 P->tw_spl[var], P->tw_sph[var]);
+    if (P->tw_ok[var]) {
+      if (!dmalloc(&P->d_sp[var], sp.size())) return bail(fail(ADI_ERR_OOM, "cudaMalloc spike tables"));
+      cudaMemcpy(P->d_sp[var], sp.data(), sp.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
   }
   // box mode (nranks > 1): the caller owns the slab buffers (adi_box_*); the patch
   // keeps only the 1D operators, factor tables and sweep checkpoints.
@@ -894,8 +1028,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     // per-warp checkpoint slots: (grid warps) x (chunks) x (state words) x 32 lanes
     int64_t words = 0;
     for (int m = 0; m < 3; m++)
-      words = std::max<int64_t>(words, (int64_t)P->sw_grid[m] * adi::SW_WARPS * ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) *
-                                           adi::sw_state_words(m, p) * 32);
+      words = std::max<int64_t>(words, (int64_t)std::max(P->sw_grid[m], P->sw_grid_tw[m]) * adi::SW_WARPS *
+                                           ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) * adi::sw_state_words(m, p) * 32);
     P->ckpt_words = (size_t)words;
     if (!dmalloc(&P->ckpt, P->ckpt_words)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
   }
@@ -1359,13 +1493,14 @@ adi_status adi_box_sweep(adi_patch P, int32_t mode, int32_t njobs, const adi_swe
     r[j] = SweepReq{J.comp, J.axis, J.in, J.out, J.iu, J.base, J.coef, {J.dims[0], J.dims[1], J.dims[2]}};
   }
   // the modified sweeps read c from the job (box layout), not from the patch
-  adi::SweepBatch B = make_batch(P, r, njobs);
+  const bool tw = twisted(P, r, njobs, mode);
+  adi::SweepBatch B = make_batch(P, r, njobs, tw ? 16 : 32);
   for (int j = 0; j < njobs; j++) B.job[j].c = jobs[j].c;
   B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
   LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
   const int64_t blocks_needed = ((int64_t)B.ntiles + adi::SW_WARPS - 1) / adi::SW_WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->sw_grid[mode]);
-  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode); });
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, tw ? P->sw_grid_tw[mode] : P->sw_grid[mode]);
+  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode, tw); });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_sweep: %s", cudaGetErrorString(e)));
   return ADI_OK;

@@ -65,29 +65,33 @@ cudaError_t Ops<ADI_P>::rhs_attrs() {
 }
 
 template <>
-void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode) {
+void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode, bool twisted) {
   const unsigned block = 32 * SW_WARPS;
-  if (mode == SW_MOD) sweep_kernel<ADI_P, SW_MOD><<<grid, block, sw_smem_bytes<SW_MOD>(), st>>>(B);
+  if (twisted && mode == SW_DER) sweep_tw_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
+  else if (twisted) sweep_tw_kernel<ADI_P, SW_MASS><<<grid, block, sw_smem_bytes<SW_MASS>(), st>>>(B);
+  else if (mode == SW_MOD) sweep_kernel<ADI_P, SW_MOD><<<grid, block, sw_smem_bytes<SW_MOD>(), st>>>(B);
   else if (mode == SW_DER) sweep_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
   else sweep_kernel<ADI_P, SW_MASS><<<grid, block, sw_smem_bytes<SW_MASS>(), st>>>(B);
 }
 
 namespace {
-template <int MODE>
-cudaError_t sweep_attr_one(int* occ) {
-  constexpr size_t smem = sw_smem_bytes<MODE>();
-  cudaError_t e = cudaFuncSetAttribute(sweep_kernel<ADI_P, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <class K>
+cudaError_t attr_occ(K kernel, size_t smem, int* occ) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, sweep_kernel<ADI_P, MODE>, 32 * SW_WARPS, smem);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kernel, 32 * SW_WARPS, smem);
 }
 }  // namespace
 
 template <>
-cudaError_t Ops<ADI_P>::sweep_attrs(int occ[3]) {
+cudaError_t Ops<ADI_P>::sweep_attrs(int occ[3], int occ_tw[3]) {
   cudaError_t e;
-  if ((e = sweep_attr_one<SW_MASS>(&occ[SW_MASS]))) return e;
-  if ((e = sweep_attr_one<SW_MOD>(&occ[SW_MOD]))) return e;
-  return sweep_attr_one<SW_DER>(&occ[SW_DER]);
+  if ((e = attr_occ(sweep_kernel<ADI_P, SW_MASS>, sw_smem_bytes<SW_MASS>(), &occ[SW_MASS]))) return e;
+  if ((e = attr_occ(sweep_kernel<ADI_P, SW_MOD>, sw_smem_bytes<SW_MOD>(), &occ[SW_MOD]))) return e;
+  if ((e = attr_occ(sweep_kernel<ADI_P, SW_DER>, sw_smem_bytes<SW_DER>(), &occ[SW_DER]))) return e;
+  if ((e = attr_occ(sweep_tw_kernel<ADI_P, SW_MASS>, sw_smem_bytes<SW_MASS>(), &occ_tw[SW_MASS]))) return e;
+  occ_tw[SW_MOD] = occ[SW_MOD];
+  return attr_occ(sweep_tw_kernel<ADI_P, SW_DER>, sw_smem_bytes<SW_DER>(), &occ_tw[SW_DER]);
 }
 
 template <>

@@ -9,6 +9,7 @@
 
 #include "rhs.cuh"
 #include "sweep.cuh"
+#include "sweep_tw.cuh"
 
 namespace adi {
 
@@ -21,10 +22,11 @@ struct Ops {
                   int s, int d);
   static cudaError_t rhs_attrs();
   // One batched sweep launch (persistent grid chosen by the caller).
-  static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode);
-  // Set the dynamic shared memory of the sweep kernels; occ[mode] = resident
-  // blocks per SM (SweepMode order: mass, modified, derivative projection).
-  static cudaError_t sweep_attrs(int occ[3]);
+  // twisted: two-segment SPIKE variant (mass / derivative modes, sweep_tw.cuh).
+  static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode, bool twisted);
+  // Set the dynamic shared memory of the sweep kernels; occ[mode] / occ_tw[mode] =
+  // resident blocks per SM (SweepMode order: mass, modified, derivative projection).
+  static cudaError_t sweep_attrs(int occ[3], int occ_tw[3]);
   // Pivot cache of one row-modified family (job 0 of B).
   static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };

@@ -96,6 +96,13 @@ struct SweepBatch {
   // derivative projection: band rows of A (full range) and its interior row
   const double* Ab;
   double kA[11];
+  // twisted (two-segment SPIKE) constant-matrix sweeps, per variant: split row m1,
+  // spike columns sp[row * P + j] (V1 above m1, W2 from m1 on) and the interface
+  // matrices Vb, Wt and K = (I - Vb Wt)^{-1} (P x P, row-major) -- sweep_tw.cuh
+  const double* sp[2];
+  int m1[2];
+  int spl[2], sph[2];  // spike entries outside patch rows [spl, sph) are below 1e-20 of the largest (dropped)
+  double vb[2][25], wt[2][25], kk[2][25];
 };
 
 __device__ __forceinline__ void sw_cp_async8(double* smem_dst, const double* gsrc) {
@@ -425,6 +432,58 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
 #pragma unroll
       for (int q = 0; q < P; q++) dv[P + q] = (r0 + q < hi) ? sl[q * 33 + lane] : 0.0;
     };
+    // Fast chunks of the constant-matrix modes (every row interior and converged):
+    // static row arrays instead of shifting windows (no register moves per row).
+    // yv[P + r] = y_{r0+r}; yv[0..P-1] = y_{r0-P..r0-1} from the recurrence state.
+    auto fwd_fast_cm = [&](const double* sl, const double* nx, const double* hd, double* yv) {
+#pragma unroll
+      for (int q = 0; q < P; q++) yv[q] = yw[P - 1 - q];
+      double uv[DER ? CH + 2 * P : 1];  // (DER) u_{r0-P+j}
+      if (DER) {
+#pragma unroll
+        for (int q = 0; q < P; q++) uv[q] = dv[q];
+#pragma unroll
+        for (int r = 0; r < CH; r++) uv[P + r] = sl[r * 33 + lane];
+#pragma unroll
+        for (int q = 0; q < P; q++) uv[P + CH + q] = nx ? nx[q * 33 + lane] : hd[q];
+      }
+#pragma unroll
+      for (int r = 0; r < CH; r++) {
+        double y;
+        if (DER) {
+          y = 0.0;
+#pragma unroll
+          for (int q = 0; q < W; q++) y = fma(B.kA[q], uv[r + q], y);
+        } else {
+          y = sl[r * 33 + lane];
+        }
+#pragma unroll
+        for (int q = P - 1; q >= 0; q--) y = fma(-kf[q], yv[P + r - 1 - q], y);
+        yv[P + r] = y;
+      }
+#pragma unroll
+      for (int q = 0; q < P; q++) yw[q] = yv[P + CH - 1 - q];
+      if (DER) {
+#pragma unroll
+        for (int q = 0; q < P; q++) dv[q] = uv[CH + q];
+      }
+    };
+    auto bwd_fast_cm = [&](const double* yv, double* y) {
+      double xv[CH + P];  // xv[r] = x_{r0+r}; xv[CH+q] = x_{r0+CH+q}
+#pragma unroll
+      for (int q = 0; q < P; q++) xv[CH + q] = xw[q];
+#pragma unroll
+      for (int r = CH - 1; r >= 0; r--) {
+        double x = yv[P + r];
+#pragma unroll
+        for (int q = P - 1; q >= 0; q--) x = fma(-kf[P + 1 + q], xv[r + 1 + q], x);
+        xv[r] = x * kf[P];
+      }
+#pragma unroll
+      for (int q = 0; q < P; q++) xw[q] = xv[q];
+#pragma unroll
+      for (int r = 0; r < CH; r++) y[r] = xv[r];
+    };
 
     // ---------------- pass 1: forward elimination, checkpoints ----------------
     // DER needs chunk c+1 resident while eliminating chunk c (window u_{k+P}).
@@ -442,8 +501,14 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       const int r0 = lo + c * CH;
       if (DER) der_prime(sl, r0);
       save_state(c);
-      if (chunk_fast(r0)) fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
-      else fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+      if (!MOD && chunk_fast(r0)) {
+        double yv[P + CH];
+        fwd_fast_cm(sl, nx, nullptr, yv);
+      } else if (chunk_fast(r0)) {
+        fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+      } else {
+        fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+      }
       __syncwarp();
       if (c + RS - 1 < nc) issue(c + RS - 1, 1);
       else sw_commit();
@@ -481,7 +546,11 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       if (DER) der_prime(sl, r0);
       double y[CH];
       double us[CH * UW];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
-      if (chunk_fast(r0)) {
+      if (!MOD && chunk_fast(r0)) {
+        double yv[P + CH];
+        fwd_fast_cm(sl, nullptr, hd, yv);
+        bwd_fast_cm(yv, y);
+      } else if (chunk_fast(r0)) {
         fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us);
         bwd_chunk(std::true_type{}, sl, r0, y, us);
       } else {

@@ -281,3 +281,21 @@ def test_derivative_projection_multi_chunk(n, p):
     eps = workloads.random_tf(N, 11, 1.0, 80.0)
     errs = _step_pair(n, p, 0.01, 2, eps, None, False)
     assert max(errs) <= TOL_STEP, errs
+
+
+@pytest.mark.parametrize("twisted", ["0", "1"])
+def test_twisted_and_single_segment_sweeps(twisted):
+    """Two-segment SPIKE sweeps (default) and one lane per fiber (ADI_SW_TWISTED=0)
+    both match the oracle; odd and even active lengths (ragged split)."""
+    import os
+    old = os.environ.get("ADI_SW_TWISTED")
+    os.environ["ADI_SW_TWISTED"] = twisted
+    try:
+        for n, p in [(30, 2), (27, 3), (41, 2)]:
+            errs, _ = _parity_run(n, p, 0.01, 2, material="phantom4")
+            assert max(errs) <= TOL_STEP, (n, p, errs)
+    finally:
+        if old is None:
+            os.environ.pop("ADI_SW_TWISTED")
+        else:
+            os.environ["ADI_SW_TWISTED"] = old
