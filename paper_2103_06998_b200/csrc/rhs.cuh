@@ -17,6 +17,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 namespace adi {
 
 // 1D operator codes of the band tables: tab[(op*N + row)*(2P+1) + q] holds the
@@ -69,6 +71,7 @@ struct RhsArgs {
   int kg0, nzout;             // output arrays hold global planes [kg0, kg0 + nzout)
   int use_sdirect;            // source amplitude given directly (sdirect) instead of signal[*step]
   double sdirect;
+  int ntx, nty, fx, fy;       // tiles per axis; interior tiles are [1, fx] x [1, fy] (the FAST launch)
   const double* tab;          // band tables, 4 ops
   const double* u[RX_MAXT];   // term inputs
   const double* a;            // tau/(2 eps^)
@@ -164,13 +167,28 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
   const int N = args.N;
   const int tid = threadIdx.x;
   const int tx = tid & 31, ty = tid >> 5;  // y-pass / output: column tx, rows 2ty, 2ty+1
-  const int bx = blockIdx.x + (FAST ? 1 : 0), by = blockIdx.y + (FAST ? 1 : 0);
-  const int i0 = bx * RX_TX, j0 = by * RX_TY;
-  if (!FAST) {
-    const bool xin = i0 >= 2 * P && i0 + RX_TX <= N - 2 * P;
-    const bool yin = j0 >= 2 * P && j0 + RX_TY <= N - 2 * P;
-    if (xin && yin) return;  // interior tile: the FAST launch owns it
+  // FAST: grid (fx, fy) over the interior tiles; general: the rim tiles, enumerated as
+  // full rows {0} u [fy+1, nty) followed by the side tiles {0} u [fx+1, ntx) of rows [1, fy]
+  int bx, by;
+  if (FAST) {
+    bx = blockIdx.x + 1;
+    by = blockIdx.y + 1;
+  } else {
+    const int e = blockIdx.x, nfull = (args.nty - args.fy) * args.ntx;
+    if (e < nfull) {
+      const int ri = e / args.ntx;
+      bx = e - ri * args.ntx;
+      by = ri == 0 ? 0 : args.fy + ri;
+    } else {
+      const int nside = args.ntx - args.fx, e2 = e - nfull, ri = e2 / nside, k = e2 - ri * nside;
+      by = 1 + ri;
+      bx = k == 0 ? 0 : args.fx + k;
+    }
   }
+  const int i0 = bx * RX_TX, j0 = by * RX_TY;
+  // (general tiles) x / y rows of the tile all Toeplitz? then that pass uses the parameter-bank stencils
+  const bool xint = FAST || (i0 >= 2 * P && i0 + RX_TX <= N - 2 * P);
+  const bool yint = FAST || (j0 >= 2 * P && j0 + RX_TY <= N - 2 * P);
   // output planes (local) [k0, k1); input planes (local) kin = k + zoff + q - P
   const int k0 = blockIdx.z * args.kchunk;
   const int k1 = min(args.nzout, k0 + args.kchunk);
@@ -288,33 +306,37 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
           __syncthreads();
         }
         // ---- x-pass: rows yy of every term, two outputs (2u, 2u+1) per task
+        auto xpass = [&](auto kx) {
 #pragma unroll
-        for (int t = 0; t < NT; t++) {
-          const int xop = Prog::op(t, 0);
+          for (int t = 0; t < NT; t++) {
+            const int xop = Prog::op(t, 0);
 #pragma unroll
-          for (int m = 0; m < (HY + 15) / 16; m++) {
-            const int yy = xrow0 + 16 * m;
-            if (m == 0 || yy < HY) {
-              const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
-              double v[2 * P + 2];
+            for (int m = 0; m < (HY + 15) / 16; m++) {
+              const int yy = xrow0 + 16 * m;
+              if (m == 0 || yy < HY) {
+                const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
+                double v[2 * P + 2];
 #pragma unroll
-              for (int q = 0; q <= P; q++) {
-                const double2 d2 = rp[q];
-                v[2 * q] = d2.x;
-                v[2 * q + 1] = d2.y;
+                for (int q = 0; q <= P; q++) {
+                  const double2 d2 = rp[q];
+                  v[2 * q] = d2.x;
+                  v[2 * q + 1] = d2.y;
+                }
+                double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+                for (int q = 0; q < W; q++) {
+                  const double c0 = decltype(kx)::value ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u) * W + q];
+                  const double c1 = decltype(kx)::value ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u + 1) * W + q];
+                  o0 = fma(c0, v[q], o0);
+                  o1 = fma(c1, v[q + 1], o1);
+                }
+                *reinterpret_cast<double2*>(sxb + (t * HY + yy) * RX_TX + 2 * u) = make_double2(o0, o1);
               }
-              double o0 = 0.0, o1 = 0.0;
-#pragma unroll
-              for (int q = 0; q < W; q++) {
-                const double c0 = FAST ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u) * W + q];
-                const double c1 = FAST ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u + 1) * W + q];
-                o0 = fma(c0, v[q], o0);
-                o1 = fma(c1, v[q + 1], o1);
-              }
-              *reinterpret_cast<double2*>(sxb + (t * HY + yy) * RX_TX + 2 * u) = make_double2(o0, o1);
             }
           }
-        }
+        };
+        if (FAST || xint) xpass(std::true_type{});
+        else xpass(std::false_type{});
         __syncthreads();  // x-pass(kin) visible; ring slot st free
         produce(kin + RX_RING);
         // ---- y-pass: rows 2ty, 2ty+1 of column tx -> z-window slot ph
@@ -325,12 +347,18 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
 #pragma unroll
           for (int q = 0; q <= W; q++) col[q] = sxb[(t * HY + 2 * ty + q) * RX_TX + tx];
           double vA = 0.0, vB = 0.0;
+          if (FAST || yint) {
 #pragma unroll
-          for (int q = 0; q < W; q++) {
-            const double cA = FAST ? args.kint[yop][q] : cys[(yop * RX_TY + 2 * ty) * W + q];
-            const double cB = FAST ? args.kint[yop][q] : cys[(yop * RX_TY + 2 * ty + 1) * W + q];
-            vA = fma(cA, col[q], vA);
-            vB = fma(cB, col[q + 1], vB);
+            for (int q = 0; q < W; q++) {
+              vA = fma(args.kint[yop][q], col[q], vA);
+              vB = fma(args.kint[yop][q], col[q + 1], vB);
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < W; q++) {  // (warp-uniform rows: broadcast reads)
+              vA = fma(cys[(yop * RX_TY + 2 * ty) * W + q], col[q], vA);
+              vB = fma(cys[(yop * RX_TY + 2 * ty + 1) * W + q], col[q + 1], vB);
+            }
           }
           w[t][0][ph] = vA;
           w[t][1][ph] = vB;
