@@ -179,9 +179,11 @@ def cpu_oracle_rate(cfg, steps: int, sample_n: int):
     return rate, dt, desc
 
 
-def dist_init():
+def dist_init(force: bool = False):
+    """torch.distributed over NCCL when launched by torchrun with N > 1 (or forced, e.g.
+    --slabs under torchrun with one process)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws > 1:
+    if ws > 1 or (force and "MASTER_ADDR" in os.environ):
         import torch.distributed as dist
 
         backend = "nccl"
@@ -287,7 +289,7 @@ class _Slabs:
         nz = self.D.nz
         self.fields = [torch.from_numpy(rng.uniform(-1.0, 1.0, size=(nz, N, N))).pin_memory() for _ in range(6)]
         self.D.set_fields(self.fields)
-        self.stream_handle = torch.cuda.current_stream(local).cuda_stream
+        self.stream_handle = self.D.stream.cuda_stream
         self.local_bytes = 6 * nz * N * N * 8
 
     def step(self, k):
@@ -319,16 +321,16 @@ class _Slabs:
 def run_ours(args, cfg):
     import torch
 
-    dist, rank, ws = dist_init()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    dist, rank, ws = dist_init(force=args.slabs)
     import paper_2103_06998_b200 as adi
 
     adi.build()
     n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
     N = n + p
     U = N ** 3
-    S = (_Whole if ws == 1 else _Slabs)(cfg, local, 1000 + rank)
+    S = (_Whole if ws == 1 and not args.slabs else _Slabs)(cfg, local, 1000 + rank)
     S.step(args.warmup)
     torch.cuda.synchronize()
     # ---------------- timed region (device-resident state) ----------------
@@ -435,6 +437,8 @@ def main():
     ap.add_argument("--oracle-n", type=int, default=48, help="n of the bounded CPU-oracle sample")
     ap.add_argument("--oracle-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true",
+                    help="use the slab-decomposed path (paper_2103_06998_b200.dist) even on one GPU")
     args = ap.parse_args()
     cfg = dict(workloads.CONFIGS[args.config])
     cfg["name"] = args.config

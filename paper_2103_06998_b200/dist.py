@@ -148,12 +148,15 @@ class DistPatch:
         self.n, self.p, self.tau, self.bc = n, p, tau, bc
         self.N = N = n + p
         self.plan = SlabPlan(N, p, nranks)
+        self.stream = None
         if backend is None:
             import paper_2103_06998_b200 as adi
             if device is None:
                 device = torch.cuda.current_device()
-            backend = adi.Patch(n, p, tau, bc, device=device, rank=rank, nranks=nranks,
-                                stream=torch.cuda.current_stream(device).cuda_stream)
+            # one CUDA stream for everything of this rank: the library's kernels, torch's
+            # copies and the NCCL collectives (which order themselves after the current stream)
+            self.stream = torch.cuda.Stream(device)
+            backend = adi.Patch(n, p, tau, bc, device=device, rank=rank, nranks=nranks, stream=self.stream.cuda_stream)
             self.device = torch.device("cuda", device)
         else:
             self.device = torch.device("cpu")
@@ -179,6 +182,10 @@ class DistPatch:
         self.step_index = 0
         self.set_materials_tf(torch.ones(N ** 3, dtype=torch.float64, device=self.device), None)
 
+    def _on_stream(self):
+        import contextlib
+        return torch.cuda.stream(self.stream) if self.stream is not None else contextlib.nullcontext()
+
     # -- layout helpers -------------------------------------------------------------
     def inner(self, t):
         return t[self.p:self.p + self.nz]
@@ -193,14 +200,22 @@ class DistPatch:
 
     # -- setup ----------------------------------------------------------------------
     def set_materials(self, eps_elem, mu_elem=None):
+        with self._on_stream():
+            return self._set_materials(eps_elem, mu_elem)
+
+    def _set_materials(self, eps_elem, mu_elem=None):
         """Element-wise eps, mu (global n^3 arrays, given on every rank) -> eps^, mu^ (D6)."""
         N = self.N
         eps_tf = torch.empty(N ** 3, dtype=torch.float64, device=self.device)
         mu_tf = torch.empty(N ** 3, dtype=torch.float64, device=self.device)
         self.B.box_materials_tf(eps_elem, mu_elem, eps_tf, mu_tf)
-        self.set_materials_tf(eps_tf, mu_tf)
+        self._set_materials_tf(eps_tf, mu_tf)
 
     def set_materials_tf(self, eps_tf, mu_tf=None):
+        with self._on_stream():
+            return self._set_materials_tf(eps_tf, mu_tf)
+
+    def _set_materials_tf(self, eps_tf, mu_tf=None):
         """Per-test-function eps^, mu^ (global N^3 arrays on every rank)."""
         N, nz, ny = self.N, self.nz, self.ny
         eps_tf = torch.as_tensor(eps_tf, dtype=torch.float64).to(self.device).reshape(-1)
@@ -235,6 +250,10 @@ class DistPatch:
                 self.iu[(s, d)] = iu
 
     def set_fields(self, fields):
+        with self._on_stream():
+            return self._set_fields(fields)
+
+    def _set_fields(self, fields):
         """Six local z-slabs (nz, N, N) (or flat), E1..H3; PEC entries forced to 0 (D1)."""
         for c in range(6):
             src = torch.as_tensor(fields[c], dtype=torch.float64).to(self.device).reshape(self.nz, self.N, self.N)
@@ -242,9 +261,17 @@ class DistPatch:
             self.B.box_pec(c, self.inner(self.F[c]), self.zdims, (0, 0, self.k0))
 
     def get_fields(self):
-        return [self.inner(f).clone() for f in self.F]
+        with self._on_stream():
+            out = [self.inner(f).clone() for f in self.F]
+        if self.stream is not None:
+            self.stream.synchronize()
+        return out
 
     def set_source(self, loads, signal):
+        with self._on_stream():
+            return self._set_source(loads, signal)
+
+    def _set_source(self, loads, signal):
         """loads: three global N^3 load vectors or None (D9); signal[m] = s((m+1/2) tau)."""
         N = self.N
         self.loads = [None, None, None]
@@ -355,6 +382,10 @@ class DistPatch:
         # the halo planes of the swapped-in buffers are refreshed by the next exchange
 
     def step(self, k: int = 1):
+        with self._on_stream():
+            self._step(k)
+
+    def _step(self, k: int):
         for _ in range(int(k)):
             self.substep(1)
             self.substep(2)
