@@ -54,9 +54,11 @@ constexpr int SW_CH_DER = ADI_SW_CH_DER, SW_RS_DER = ADI_SW_RS_DER;
 __host__ __device__ constexpr int sw_ch(int mode) { return mode == SW_MOD ? SW_CH_MOD : mode == SW_DER ? SW_CH_DER : SW_CH_MASS; }
 __host__ __device__ constexpr int sw_rs(int mode) { return mode == SW_MOD ? SW_RS_MOD : mode == SW_DER ? SW_RS_DER : SW_RS_MASS; }
 __host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? 3 : mode == SW_DER ? 2 : 1; }
-// checkpoint words per chunk: y window (P); MOD adds pivots (P) and U entries (P*P); DER adds the u window (P)
+// checkpoint words per chunk: y window (P); MOD adds the U entries u_{k-m,k-m+j}, j < P
+// (P(P-1); the pivots and u_{k-m,k-m+P} = M + c S entries are re-read from the pivot
+// cache and c); DER adds the u window (P)
 __host__ __device__ constexpr int sw_state_words(int mode, int P) {
-  return mode == SW_MOD ? P * (P + 2) : mode == SW_DER ? 2 * P : P;
+  return mode == SW_MOD ? P * P : mode == SW_DER ? 2 * P : P;
 }
 template <int MODE>
 constexpr size_t sw_smem_bytes() {
@@ -333,26 +335,27 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       for (int m = 0; m < P; m++) p[m * 32] = yw[m];
       if (MOD) {
 #pragma unroll
-        for (int m = 0; m < P; m++) {
-          p[(P + m) * 32] = iw[m];
+        for (int m = 0; m < P; m++)
 #pragma unroll
-          for (int j = 0; j < P; j++) p[(2 * P + m * P + j) * 32] = uw[m][j];
-        }
+          for (int j = 0; j < P - 1; j++) p[(P + m * (P - 1) + j) * 32] = uw[m][j];
       }
       if (DER) {  // u_{r0-P..r0-1} = dv[0..P-1] at the chunk start
 #pragma unroll
         for (int q = 0; q < P; q++) p[(P + q) * 32] = dv[q];
       }
     };
-    auto set_state = [&](const double* p) {
+    // pv[m-1], pc[m-1]: pivot 1/u and c of patch row r0 - m (MOD; loaded ahead of time)
+    auto set_state = [&](const double* p, const double* pv, const double* pc, int r0) {
 #pragma unroll
       for (int m = 0; m < P; m++) yw[m] = p[m];
       if (MOD) {
 #pragma unroll
         for (int m = 0; m < P; m++) {
-          iw[m] = p[P + m];
 #pragma unroll
-          for (int j = 0; j < P; j++) uw[m][j] = p[2 * P + m * P + j];
+          for (int j = 0; j < P - 1; j++) uw[m][j] = p[P + m * (P - 1) + j];
+          const int row = r0 - 1 - m;
+          iw[m] = row >= lo ? pv[m] : 0.0;
+          uw[m][P - 1] = row >= lo ? mod_entry(std::false_type{}, row, pc[m], 2 * P) : 0.0;
         }
       }
       if (DER) {
@@ -522,8 +525,21 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
     for (int q = 0; q < P; q++) xw[q] = 0.0;
     double hd[DER ? P : 1];  // (DER) u of the first P rows of chunk c+1
     double nxt[SWD];         // checkpoint of the next chunk to process, loaded one iteration ahead
+    double pv[MOD ? P : 1], pc[MOD ? P : 1];  // (MOD) pivots and c of the P rows before that chunk
+    auto load_prev = [&](int c) {
 #pragma unroll
-    for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(nc - 1) * SWD + q) * 32];
+      for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)c * SWD + q) * 32];
+      if (MOD) {
+        const int r0 = lo + c * CH;
+#pragma unroll
+        for (int m = 0; m < P; m++) {
+          const int row = max(r0 - 1 - m, lo);
+          pv[m] = __ldg(src[2] + base + (int64_t)row * stride);
+          pc[m] = __ldg(src[1] + base + (int64_t)row * stride);
+        }
+      }
+    };
+    load_prev(nc - 1);
     if (DER) {
 #pragma unroll
       for (int c = 0; c < RS - 1; c++) {
@@ -538,11 +554,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       __syncwarp();
       double* sl = ring + (c % RS) * SLOT;
       const int r0 = lo + c * CH;
-      set_state(nxt);
-      if (c > 0) {
-#pragma unroll
-        for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)(c - 1) * SWD + q) * 32];
-      }
+      set_state(nxt, pv, pc, r0);
+      if (c > 0) load_prev(c - 1);
       if (DER) der_prime(sl, r0);
       double y[CH];
       double us[CH * UW];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)

@@ -133,3 +133,34 @@ def test_dist_decomposition_invariance_bitwise():
     outs = [run_ranks(R, 14, 2, 0.01, 2)[0] for R in (1, 2, 4)]
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+def test_box_mode_abi_contract():
+    """Box-mode patch (nranks > 1): layout = balanced z-slab; whole-patch calls are
+    ADI_ERR_STATE; box calls validate their arguments (ADI_ERR_ARG)."""
+    import paper_2103_06998_b200 as adi
+
+    n, p = 10, 2
+    N = n + p
+    for r in range(3):
+        B = adi.Patch(n, p, 0.01, rank=r, nranks=3)
+        assert B.layout() == (N, r * N // 3, (r + 1) * N // 3)
+    B = adi.Patch(n, p, 0.01, rank=1, nranks=3)
+    with pytest.raises(adi.AdiError) as e:
+        B.step(1)
+    assert e.value.status == adi.ADI_ERR_STATE
+    with pytest.raises(adi.AdiError) as e:
+        B.set_fields([np.zeros(N ** 3)] * 6)
+    assert e.value.status == adi.ADI_ERR_STATE
+    t = torch.zeros(N, N, 4, dtype=torch.float64, device="cuda")
+    with pytest.raises(adi.AdiError) as e:  # dims[axis] must equal N
+        B.box_sweep(0, [dict(dims=(N, N, 4), axis=2, comp=3, **{"in": t}, out=t)])
+    assert e.value.status == adi.ADI_ERR_ARG
+    with pytest.raises(adi.AdiError) as e:  # box outside the array
+        B.box_copy(t, (N, N, 4), (0, 0, 1), t, (N, N, 4), (0, 0, 0), (N, N, 4))
+    assert e.value.status == adi.ADI_ERR_ARG
+    with pytest.raises(adi.AdiError) as e:
+        B.box_rhs(0, 3, 0, [t] * 4, 4, 0, 0, 4, t, t, t, None, 0.0, t)
+    assert e.value.status == adi.ADI_ERR_ARG
+    with pytest.raises(adi.AdiError):
+        adi.Patch(n, p, 0.01, rank=3, nranks=3)
