@@ -1032,7 +1032,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     int64_t words = 0;
     for (int m = 0; m < 3; m++)
       words = std::max<int64_t>(words, (int64_t)std::max(P->sw_grid[m], P->sw_grid_tw[m]) * adi::SW_WARPS *
-                                           ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) * adi::sw_state_words(m, p) * 32);
+                                           ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) *
+                                           std::max(adi::sw_state_words(m, p), adi::sw_state_words_tw(m, p)) * 32);
     P->ckpt_words = (size_t)words;
     if (!dmalloc(&P->ckpt, P->ckpt_words)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
   }

@@ -56,10 +56,12 @@ __host__ __device__ constexpr int sw_rs(int mode) { return mode == SW_MOD ? SW_R
 __host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? 3 : mode == SW_DER ? 2 : 1; }
 // checkpoint words per chunk: y window (P); MOD adds the U entries u_{k-m,k-m+j}, j < P
 // (P(P-1); the pivots and u_{k-m,k-m+P} = M + c S entries are re-read from the pivot
-// cache and c); DER adds the u window (P)
+// cache and c); DER: y only (the u window is re-read from u)
 __host__ __device__ constexpr int sw_state_words(int mode, int P) {
-  return mode == SW_MOD ? P * P : mode == SW_DER ? 2 * P : P;
+  return mode == SW_MOD ? P * P : P;
 }
+// (the twisted kernel keeps the u window in its checkpoints)
+__host__ __device__ constexpr int sw_state_words_tw(int mode, int P) { return mode == SW_DER ? 2 * P : P; }
 template <int MODE>
 constexpr size_t sw_smem_bytes() {
   return sizeof(double) * (size_t)SW_WARPS * sw_rs(MODE) * sw_na(MODE) * sw_ch(MODE) * 33;
@@ -339,10 +341,6 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
 #pragma unroll
           for (int j = 0; j < P - 1; j++) p[(P + m * (P - 1) + j) * 32] = uw[m][j];
       }
-      if (DER) {  // u_{r0-P..r0-1} = dv[0..P-1] at the chunk start
-#pragma unroll
-        for (int q = 0; q < P; q++) p[(P + q) * 32] = dv[q];
-      }
     };
     // pv[m-1], pc[m-1]: pivot 1/u and c of patch row r0 - m (MOD; loaded ahead of time)
     auto set_state = [&](const double* p, const double* pv, const double* pc, int r0) {
@@ -358,9 +356,9 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
           uw[m][P - 1] = row >= lo ? mod_entry(std::false_type{}, row, pc[m], 2 * P) : 0.0;
         }
       }
-      if (DER) {
+      if (DER) {  // dv[q] = u_{r0-P+q}: pv[m] holds u at row r0-1-m
 #pragma unroll
-        for (int q = 0; q < P; q++) dv[q] = p[P + q];
+        for (int q = 0; q < P; q++) dv[q] = (r0 - P + q >= lo) ? pv[P - 1 - q] : 0.0;
       }
     };
     // chunk rows all in [lo,hi) and in the Toeplitz / converged range?
@@ -525,17 +523,21 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
     for (int q = 0; q < P; q++) xw[q] = 0.0;
     double hd[DER ? P : 1];  // (DER) u of the first P rows of chunk c+1
     double nxt[SWD];         // checkpoint of the next chunk to process, loaded one iteration ahead
-    double pv[MOD ? P : 1], pc[MOD ? P : 1];  // (MOD) pivots and c of the P rows before that chunk
+    double pv[MOD || DER ? P : 1], pc[MOD ? P : 1];  // pivots and c (MOD) / u (DER) of the P rows before that chunk
     auto load_prev = [&](int c) {
 #pragma unroll
       for (int q = 0; q < SWD; q++) nxt[q] = ck[((size_t)c * SWD + q) * 32];
-      if (MOD) {
+      if (MOD || DER) {
         const int r0 = lo + c * CH;
 #pragma unroll
         for (int m = 0; m < P; m++) {
           const int row = max(r0 - 1 - m, lo);
-          pv[m] = __ldg(src[2] + base + (int64_t)row * stride);
-          pc[m] = __ldg(src[1] + base + (int64_t)row * stride);
+          if (MOD) {
+            pv[m] = __ldg(src[2] + base + (int64_t)row * stride);
+            pc[m] = __ldg(src[1] + base + (int64_t)row * stride);
+          } else {
+            pv[m] = __ldg(src[0] + base + (int64_t)row * stride);
+          }
         }
       }
     };

@@ -33,7 +33,7 @@ sweep_tw_kernel(const __grid_constant__ SweepBatch B) {
   constexpr int CH = sw_ch(MODE), RS = sw_rs(MODE), NA = sw_na(MODE);
   constexpr int W = 2 * P + 1;
   constexpr int SLOT = NA * CH * 33;
-  constexpr int SWD = sw_state_words(MODE, P);
+  constexpr int SWD = sw_state_words_tw(MODE, P);
   static_assert(!DER || (RS >= 3 && CH >= P), "derivative mode needs the next chunk resident");
   constexpr int FPI = 32 / CH;
   extern __shared__ double sw_smem[];
