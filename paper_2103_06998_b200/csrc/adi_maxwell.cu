@@ -170,6 +170,10 @@ struct adi_patch_s {
   double* G[3] = {};
   double *a = nullptr, *b = nullptr, *c = nullptr, *epsh = nullptr, *muh = nullptr;
   double* ckpt = nullptr;   // per-warp checkpoint slots of the sweep kernels
+  double* ckpt2 = nullptr;  // ... of a sweep running concurrently on stream2
+  cudaStream_t stream2 = nullptr;  // side branch of the step graph (first H projection)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int overlap = 0;          // ADI_OVERLAP=1: first H projection as a concurrent graph branch (measured slower: L2 contention)
   size_t ckpt_words = 0;
   double* iu[6] = {};       // cached pivots 1/u_kk of the six row-modified families (s, d)
   int hk[2] = {0, 0}, tk[2] = {0, 0};  // mass factor rows equal to the interior row
@@ -459,15 +463,18 @@ bool twisted(adi_patch P, const SweepReq* req, int nreq, int mode) {
   return true;
 }
 
-adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode) {
+adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode, cudaStream_t st = nullptr,
+                         double* ckpt = nullptr) {
   const bool tw = twisted(P, req, nreq, mode);
   adi::SweepBatch B = make_batch(P, req, nreq, tw ? 16 : 32);
+  if (ckpt) B.ckpt = ckpt;
+  if (!st) st = P->stream;
   B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
   LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
   const int64_t warps_needed = B.ntiles;
   const int64_t blocks_needed = (warps_needed + adi::SW_WARPS - 1) / adi::SW_WARPS;
   const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, tw ? P->sw_grid_tw[mode] : P->sw_grid[mode]);
-  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode, tw); });
+  with_degree(P->p, [&](auto ops) { ops.sweep(st, grid, B, mode, tw); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }
@@ -546,16 +553,21 @@ adi_status solve_h_all(adi_patch P, double* const u[3]) {
 // with D_a = M_a^{-1} A_a along axis a (M^{-1}(M (x) A (x) M) = I (x) M^{-1}A (x) I;
 // H rows are unrestricted, PEC-eliminated E entries are stored zeros).  Two
 // batched derivative-projection launches (three components each).
-adi_status h_update_uniform_mu(adi_patch P, int s, const double* const H[3], const double* const Eo[3],
-                               const double* const En[3], double* const G[3]) {
+// first projection (depends only on the substep's starting fields): may run on a side stream
+adi_status h_update_first(adi_patch P, int s, const double* const H[3], const double* const Eo[3], double* const G[3],
+                          cudaStream_t st = nullptr, double* ckpt = nullptr) {
   const double b = P->b_scalar;
   SweepReq r[3];
   for (int d = 0; d < 3; d++) {
     const int a1 = s == 1 ? (d + 1) % 3 : (d + 2) % 3, x1 = s == 1 ? (d + 2) % 3 : (d + 1) % 3;
     r[d] = SweepReq{3 + d, a1, Eo[x1], G[d], nullptr, H[d], s == 1 ? -b : b};
   }
-  adi_status st = launch_sweeps(P, r, 3, adi::SW_DER);
-  if (st) return st;
+  return launch_sweeps(P, r, 3, adi::SW_DER, st, ckpt);
+}
+
+adi_status h_update_second(adi_patch P, int s, const double* const En[3], double* const G[3]) {
+  const double b = P->b_scalar;
+  SweepReq r[3];
   for (int d = 0; d < 3; d++) {
     const int a2 = s == 1 ? (d + 2) % 3 : (d + 1) % 3, x2 = s == 1 ? (d + 1) % 3 : (d + 2) % 3;
     r[d] = SweepReq{3 + d, a2, En[x2], G[d], nullptr, G[d], s == 1 ? b : -b};
@@ -565,15 +577,34 @@ adi_status h_update_uniform_mu(adi_patch P, int s, const double* const H[3], con
 
 // One substep (ALG-2 / ALG-7): RHS_E -> E solves -> RHS_H -> H solves, then
 // rotate buffers (new E lives in R, new H in G).
+adi_status h_update_uniform_mu(adi_patch P, int s, const double* const H[3], const double* const Eo[3],
+                               const double* const En[3], double* const G[3]) {
+  adi_status st = h_update_first(P, s, H, Eo, G);
+  return st ? st : h_update_second(P, s, En, G);
+}
+
 adi_status substep(adi_patch P, int s) {
   adi_status st;
   const double* E[3] = {P->F[0], P->F[1], P->F[2]};
   const double* H[3] = {P->F[3], P->F[4], P->F[5]};
+  // uniform mu: the first H projection needs only the substep's starting fields, so it
+  // runs as a concurrent graph branch (side stream, own checkpoints) beside the E path
+  // -- the latency-bound sweeps leave issue slots and bandwidth to share.
+  const bool fork = P->mu_uniform && !P->h_general && P->overlap && !P->timing;
+  if (fork) {
+    CUDA_TRY(cudaEventRecord(P->ev_fork, P->stream));
+    CUDA_TRY(cudaStreamWaitEvent(P->stream2, P->ev_fork, 0));
+    if ((st = h_update_first(P, s, H, E, P->G, P->stream2, P->ckpt2))) return st;
+    CUDA_TRY(cudaEventRecord(P->ev_join, P->stream2));
+  }
   for (int d = 0; d < 3; d++)
     if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
   if ((st = solve_e_range(P, s, 0, 3, P->R, P->R))) return st;
   const double* En[3] = {P->R[0], P->R[1], P->R[2]};
-  if (P->mu_uniform && !P->h_general) {
+  if (fork) {
+    CUDA_TRY(cudaStreamWaitEvent(P->stream, P->ev_join, 0));
+    if ((st = h_update_second(P, s, En, P->G))) return st;
+  } else if (P->mu_uniform && !P->h_general) {
     if ((st = h_update_uniform_mu(P, s, H, E, En, P->G))) return st;
   } else {
     for (int d = 0; d < 3; d++)
@@ -834,7 +865,10 @@ void adi_destroy(adi_patch P) {
   for (int v = 0; v < 2; v++) f(P->d_fac[v]), f(P->d_Mb[v]), f(P->d_Sb[v]), f(P->d_sp[v]);
   for (int i = 0; i < 6; i++) f(P->F[i]);
   for (int i = 0; i < 3; i++) f(P->R[i]), f(P->G[i]), f(P->load[i]);
-  f(P->a), f(P->b), f(P->c), f(P->epsh), f(P->muh), f(P->ckpt), f(P->signal), f(P->d_step);
+  f(P->a), f(P->b), f(P->c), f(P->epsh), f(P->muh), f(P->ckpt), f(P->ckpt2), f(P->signal), f(P->d_step);
+  if (P->stream2) cudaStreamDestroy(P->stream2);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join) cudaEventDestroy(P->ev_join);
   for (int i = 0; i < 6; i++) f(P->iu[i]);
   for (auto& e : P->ev_used) cudaEventDestroy(e.second.first), cudaEventDestroy(e.second.second);
   for (auto& e : P->ev_free) cudaEventDestroy(e);
@@ -882,6 +916,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_SW_BPS_DER")) P->sw_bps[2] = atoi(s);
   if (const char* s = getenv("ADI_H_GENERAL")) P->h_general = atoi(s);
   if (const char* s = getenv("ADI_SW_TWISTED")) P->use_tw = atoi(s);
+  if (const char* s = getenv("ADI_OVERLAP")) P->overlap = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   {
@@ -1035,7 +1070,12 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
                                            ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) *
                                            std::max(adi::sw_state_words(m, p), adi::sw_state_words_tw(m, p)) * 32);
     P->ckpt_words = (size_t)words;
-    if (!dmalloc(&P->ckpt, P->ckpt_words)) return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
+    if (!dmalloc(&P->ckpt, P->ckpt_words) || !dmalloc(&P->ckpt2, P->ckpt_words))
+      return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
+    if (cudaStreamCreateWithFlags(&P->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(ADI_ERR_CUDA, "side stream / events"));
   }
   if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));
   cudaMemset(P->d_step, 0, sizeof(int64_t));
