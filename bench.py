@@ -434,8 +434,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c5", choices=sorted(workloads.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--oracle-n", type=int, default=48, help="n of the bounded CPU-oracle sample")
-    ap.add_argument("--oracle-steps", type=int, default=2)
+    ap.add_argument("--oracle-n", type=int, default=64,
+                    help="n of the bounded CPU-oracle sample (c5 recipe at n=64: ~2 s per oracle step)")
+    ap.add_argument("--oracle-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="use the slab-decomposed path (paper_2103_06998_b200.dist) even on one GPU")

@@ -299,3 +299,47 @@ def test_twisted_and_single_segment_sweeps(twisted):
             os.environ.pop("ADI_SW_TWISTED")
         else:
             os.environ["ADI_SW_TWISTED"] = old
+
+
+def test_c3_full_size_one_step():
+    """c3 at full size (64^3 elements, p=3, N=67 odd: cp.async halo path), phantom with
+    +-5% noise and the Gaussian-pulse dipole, one step against the oracle."""
+    cfg = workloads.CONFIGS["c3"]
+    errs, _ = _parity_run(cfg["n"], cfg["p"], cfg["tau"], 1, material="phantom3", source="pulse")
+    assert max(errs) <= TOL_STEP, errs
+
+
+def _cyc(f, n):
+    """Relabel (x1,x2,x3) -> (x2,x3,x1) of an n^3 array (x fastest): new[j,k,i] = old[i,j,k]."""
+    u = np.asarray(f).reshape(n, n, n)
+    return np.ascontiguousarray(u.transpose(2, 0, 1)).reshape(-1)
+
+
+def test_c5_full_size_cyclic_equivariance():
+    """c5 at full size (512^3, N = 514, the bench configuration) cannot be stepped by the
+    oracle in test time; instead the property P8 that holds at any size: relabelling the axes
+    (x1,x2,x3) -> (x2,x3,x1) together with the components (material included) commutes with
+    the GPU step (to rounding: the sweeps and stencil passes run along other axes)."""
+    cfg = workloads.CONFIGS["c5"]
+    n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
+    N = n + p
+    eps = workloads.element_eps(n, cfg["material"])
+    f = workloads.random_fields(N, 31)
+    G = adi.Patch(n, p, tau)
+    G.set_materials(eps)
+    G.set_fields(f)
+    G.step(1)
+    out = G.get_fields()
+    g = [None] * 6
+    for c in range(3):
+        g[(c + 2) % 3] = _cyc(f[c], N)
+        g[3 + (c + 2) % 3] = _cyc(f[3 + c], N)
+    del f
+    G.set_materials(_cyc(eps, n))
+    G.set_fields(g)
+    del g
+    G.step(1)
+    got = G.get_fields()
+    for c in range(3):
+        assert rel(got[(c + 2) % 3], _cyc(out[c], N)) <= 1e-12, c
+        assert rel(got[3 + (c + 2) % 3], _cyc(out[3 + c], N)) <= 1e-12, c
