@@ -310,10 +310,14 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
 #pragma unroll
           for (int t = 0; t < NT; t++) {
             const int xop = Prog::op(t, 0);
+            // rows 0..15: one per thread; the 2P halo rows 16..HY-1 (32P tasks) go to a
+            // different group of threads for every term, so the warps stay balanced at the barrier
+            static_assert(HY - 16 <= 16, "x-pass task map assumes at most 16 extra rows");
 #pragma unroll
-            for (int m = 0; m < (HY + 15) / 16; m++) {
-              const int yy = xrow0 + 16 * m;
-              if (m == 0 || yy < HY) {
+            for (int m = 0; m < 2; m++) {
+              const int ex = (tid - 64 * t + 4 * RX_THREADS) % RX_THREADS;  // extra-task index of this thread
+              const int yy = m == 0 ? xrow0 : 16 + (ex >> 4);
+              if (m == 0 || ex < (HY - 16) * 16) {
                 const double2* rp = reinterpret_cast<const double2*>(slot + t * PLANEP + yy * HX + 2 * u);
                 double v[2 * P + 2];
 #pragma unroll
