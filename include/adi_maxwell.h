@@ -118,6 +118,14 @@ adi_status adi_set_point_source(adi_patch patch, int32_t comp, double xs, double
  * ADI_ERR_STATE before adi_set_fields. */
 adi_status adi_step(adi_patch patch, int64_t k);
 
+/* Order of the three sweeps of each E solve (variant V1):
+ * 0 (default): the row-modified (stiffened) axis first, then the two mass sweeps in
+ *   ascending order (D7) -- equal to the row-modified global system for any material;
+ * 1: the paper's main-text order x -> y -> z, the modified matrix at the
+ *   stiffened axis -- exact only when c does not vary along the axes swept before it.
+ * ADI_ERR_ARG for other values. */
+adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
+
 /* Block until all work queued on the patch stream has finished. */
 adi_status adi_synchronize(adi_patch patch);
 

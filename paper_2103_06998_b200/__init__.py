@@ -39,7 +39,7 @@ EXPORTS = [
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
-    "adi_box_materials_tf",
+    "adi_box_materials_tf", "adi_set_sweep_order",
 ]
 
 
@@ -142,6 +142,7 @@ def lib():
                                       C.c_void_p]
             L.adi_box_pec.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, i64x3, i64x3]
             L.adi_box_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_set_sweep_order.argtypes = [C.c_void_p, C.c_int32]
             _lib = L
         return _lib
 
@@ -257,6 +258,10 @@ class Patch:
     @property
     def stream(self) -> int:
         return int(self._L.adi_stream(self.h) or 0)
+
+    def set_sweep_order(self, order: int):
+        """0: stiffened axis first (D7, default); 1: paper-literal x -> y -> z (V1)."""
+        self._check(self._L.adi_set_sweep_order(self.h, int(order)))
 
     def set_timing(self, enable: bool):
         self._check(self._L.adi_set_timing(self.h, int(bool(enable))))

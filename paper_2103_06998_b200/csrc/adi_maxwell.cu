@@ -173,6 +173,7 @@ struct adi_patch_s {
   double* ckpt2 = nullptr;  // ... of a sweep running concurrently on stream2
   cudaStream_t stream2 = nullptr;  // side branch of the step graph (first H projection)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int sweep_order = 0;      // 0: stiffened axis first (D7); 1: paper-literal x->y->z (V1, NEXT-2)
   int overlap = 0;          // ADI_OVERLAP=1: first H projection as a concurrent graph branch (measured slower: L2 contention)
   size_t ckpt_words = 0;
   double* iu[6] = {};       // cached pivots 1/u_kk of the six row-modified families (s, d)
@@ -511,6 +512,24 @@ int family(int s, int d) { return (s - 1) * 3 + d; }
 adi_status solve_e_range(adi_patch P, int s, int d0, int d1, const double* const in[3], double* const out[3]) {
   SweepReq r[3];
   int n = 0;
+  if (P->sweep_order == 1) {
+    // NEXT-2 variant V1: the paper's main-text order x -> y -> z with the
+    // row-modified matrix at the stiffened axis; exact only when c does not vary along
+    // the axes swept before it.  Per stage one modified + mass launches.
+    for (int ax = 0; ax < 3; ax++) {
+      SweepReq rm[3], rs[3];
+      int nm = 0, ns = 0;
+      for (int d = d0; d < d1; d++) {
+        const double* src = ax == 0 ? in[d] : out[d];
+        if (ax == stiff_axis(s, d)) rm[nm++] = SweepReq{d, ax, src, out[d], P->iu[family(s, d)]};
+        else rs[ns++] = SweepReq{d, ax, src, out[d], nullptr};
+      }
+      adi_status st;
+      if (nm && (st = launch_sweeps(P, rm, nm, adi::SW_MOD))) return st;
+      if (ns && (st = launch_sweeps(P, rs, ns, adi::SW_MASS))) return st;
+    }
+    return ADI_OK;
+  }
   for (int d = d0; d < d1; d++) r[n++] = SweepReq{d, stiff_axis(s, d), in[d], out[d], P->iu[family(s, d)]};
   adi_status st = launch_sweeps(P, r, n, adi::SW_MOD);
   if (st) return st;
@@ -1664,6 +1683,14 @@ adi_status adi_box_materials_tf(adi_patch P, const double* eps_elem, const doubl
   cudaFree(de);
   cudaFree(dw);
   return poison(P, st);
+}
+
+adi_status adi_set_sweep_order(adi_patch P, int32_t order) {
+  CHECK_PATCH(P);
+  if (order != 0 && order != 1) return fail(ADI_ERR_ARG, "adi_set_sweep_order: order %d not 0 or 1", order);
+  drop_graph(P);
+  P->sweep_order = order;
+  return ADI_OK;
 }
 
 }  // extern "C"

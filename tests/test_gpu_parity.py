@@ -343,3 +343,30 @@ def test_c5_full_size_cyclic_equivariance():
     for c in range(3):
         assert rel(got[(c + 2) % 3], _cyc(out[c], N)) <= 1e-12, c
         assert rel(got[3 + (c + 2) % 3], _cyc(out[3 + c], N)) <= 1e-12, c
+
+
+def test_sweep_order_variant_v1():
+    """NEXT-2 variant V1 (paper-literal x -> y -> z order): the GPU matches the oracle's V1;
+    with per-voxel material it differs from the D7 result (the order matters),
+    with uniform material both orders agree."""
+    n, p, tau = 12, 2, 0.02
+    N = n + p
+    eps = workloads.element_eps(n, "random", seed=3)
+    f = workloads.random_fields(N, 41)
+    res = {}
+    for order in (0, 1):
+        G = adi.Patch(n, p, tau)
+        G.set_sweep_order(order)
+        O = oracle.Patch(n, p, tau)
+        O.set_order_variant(order)
+        for X in (G, O):
+            X.set_materials(eps)
+            X.set_fields(f)
+            X.step(2)
+        got, ref = G.get_fields(), O.get_fields()
+        assert max(rel(a, b) for a, b in zip(got, ref)) <= TOL_STEP
+        res[order] = got
+    assert max(rel(a, b) for a, b in zip(res[1][:3], res[0][:3])) > 1e-6
+    G = adi.Patch(n, p, tau)
+    with pytest.raises(adi.AdiError):
+        G.set_sweep_order(2)
