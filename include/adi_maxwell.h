@@ -126,6 +126,11 @@ adi_status adi_step(adi_patch patch, int64_t k);
  * ADI_ERR_ARG for other values. */
 adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
 
+/* On-device diagnostic: out[c] = f_c^T (M (x) M (x) M) f_c for the six
+ * fields and out[6] = 1/2 sum_c out[c], the discrete M-norm energy 1/2 (e^T M e + h^T M h)
+ * (conserved by the curl part of the scheme).  Synchronises.  Whole patches only. */
+adi_status adi_energy(adi_patch patch, double out[7]);
+
 /* Block until all work queued on the patch stream has finished. */
 adi_status adi_synchronize(adi_patch patch);
 

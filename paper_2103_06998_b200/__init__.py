@@ -39,7 +39,7 @@ EXPORTS = [
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
-    "adi_box_materials_tf", "adi_set_sweep_order",
+    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy",
 ]
 
 
@@ -143,6 +143,7 @@ def lib():
             L.adi_box_pec.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, i64x3, i64x3]
             L.adi_box_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.adi_set_sweep_order.argtypes = [C.c_void_p, C.c_int32]
+            L.adi_energy.argtypes = [C.c_void_p, C.c_void_p]
             _lib = L
         return _lib
 
@@ -262,6 +263,12 @@ class Patch:
     def set_sweep_order(self, order: int):
         """0: stiffened axis first (D7, default); 1: paper-literal x -> y -> z (V1)."""
         self._check(self._L.adi_set_sweep_order(self.h, int(order)))
+
+    def energy(self):
+        """(per-field f^T M^3 f [6], M-norm energy 1/2 sum) -- on-device diagnostic."""
+        out = (C.c_double * 7)()
+        self._check(self._L.adi_energy(self.h, out))
+        return [out[c] for c in range(6)], out[6]
 
     def set_timing(self, enable: bool):
         self._check(self._L.adi_set_timing(self.h, int(bool(enable))))

@@ -1693,4 +1693,24 @@ adi_status adi_set_sweep_order(adi_patch P, int32_t order) {
   return ADI_OK;
 }
 
+adi_status adi_energy(adi_patch P, double out[7]) {
+  CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_energy needs the whole patch");
+  if (!out) return fail(ADI_ERR_ARG, "adi_energy: out is NULL");
+  double* acc;
+  CUDA_TRY(cudaMallocAsync(&acc, 6 * sizeof(double), P->stream));
+  CUDA_TRY(cudaMemsetAsync(acc, 0, 6 * sizeof(double), P->stream));
+  for (int c = 0; c < 6; c++)
+    adi::mnorm_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->F[c], P->d_tab + (size_t)adi::OP_M * P->N * P->W, P->N,
+                                                         P->p, acc + c);
+  double h[6];
+  CUDA_TRY(cudaMemcpyAsync(h, acc, sizeof h, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaFreeAsync(acc, P->stream));
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_energy: %s", cudaGetErrorString(e)));
+  out[6] = 0.0;
+  for (int c = 0; c < 6; c++) out[c] = h[c], out[6] += 0.5 * h[c];
+  return ADI_OK;
+}
+
 }  // extern "C"

@@ -101,4 +101,42 @@ __global__ void pec_box_kernel(double* __restrict__ u, int64_t nx, int64_t ny, i
   }
 }
 
+// sum over the patch of u (.) ((M (x) M (x) M) u) (the M-norm squared; diagnostic, not on the
+// step path): direct (2p+1)^3 stencil from the band table of M, block reduction, one atomic per block
+__global__ void mnorm_kernel(const double* __restrict__ u, const double* __restrict__ tabM, int N, int p,
+                             double* __restrict__ acc) {
+  const int W = 2 * p + 1;
+  const int64_t U = (int64_t)N * N * N;
+  double s = 0.0;
+  for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < U; I += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(I % N), j = (int)((I / N) % N), k = (int)(I / ((int64_t)N * N));
+    double v = 0.0;
+    for (int c = 0; c < W; c++) {
+      const int o = k - p + c;
+      if (o < 0 || o >= N) continue;
+      const double mz = tabM[(int64_t)k * W + c];
+      for (int b = 0; b < W; b++) {
+        const int m = j - p + b;
+        if (m < 0 || m >= N) continue;
+        const double myz = mz * tabM[(int64_t)j * W + b];
+        const double* row = u + (int64_t)N * (m + (int64_t)N * o);
+        for (int a = 0; a < W; a++) {
+          const int l = i - p + a;
+          if (l < 0 || l >= N) continue;
+          v = fma(myz * tabM[(int64_t)i * W + a], row[l], v);
+        }
+      }
+    }
+    s = fma(u[I], v, s);
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) atomicAdd(acc, red[0]);
+}
+
 }  // namespace adi

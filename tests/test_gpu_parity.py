@@ -370,3 +370,24 @@ def test_sweep_order_variant_v1():
     G = adi.Patch(n, p, tau)
     with pytest.raises(adi.AdiError):
         G.set_sweep_order(2)
+
+
+def test_energy_diagnostic():
+    """NEXT-3 diagnostic: f^T (M x M x M) f per field on the device equals the dense Kronecker
+    product with the oracle's matrices; for eps = mu = 1 the energy stays bounded by its
+    initial value over many steps (unconditional stability, P5)."""
+    n, p, tau = 7, 2, 0.05
+    N = n + p
+    f = workloads.random_fields(N, 51)
+    G = adi.Patch(n, p, tau)
+    G.set_fields(f)
+    per, tot = G.energy()
+    M = oracle.Patch(n, p, tau).matrices()[0]
+    K = np.kron(np.kron(M, M), M)  # (z, y, x) ordering of the flat index i + N(j + N k)
+    g = G.get_fields()  # PEC-zeroed copies
+    for c in range(6):
+        ref = g[c] @ (K @ g[c])
+        assert abs(per[c] - ref) <= 1e-12 * abs(ref)
+    assert abs(tot - 0.5 * sum(per)) <= 1e-14 * tot
+    G.step(50)
+    assert G.energy()[1] <= tot * (1 + 1e-2)
