@@ -391,3 +391,28 @@ def test_energy_diagnostic():
     assert abs(tot - 0.5 * sum(per)) <= 1e-14 * tot
     G.step(50)
     assert G.energy()[1] <= tot * (1 + 1e-2)
+
+
+def test_c2_full_config_parity_and_temporal_order():
+    """c2 exactly as BASELINE.json states it: 32^3 elements, p=2, u_A initial data (D10),
+    100 steps at tau = 1e-2 against the oracle (<= 1e-10 per field); then the GPU alone over
+    the tau sweep {1e-2, 5e-3, 2.5e-3} at the common time t = 0.25 shows second order
+    (P4 on the device at full size)."""
+    cfg = workloads.CONFIGS["c2"]
+    n, p = cfg["n"], cfg["p"]
+    errs, _ = _parity_run(n, p, 1e-2, 100, init="uA")
+    assert max(errs) <= TOL_STEP, errs
+    O = oracle.Patch(n, p, 1e-2)
+    O.project_uA(0.0)
+    f0 = O.get_fields()
+    runs = []
+    for tau, st in [(1e-2, 25), (5e-3, 50), (2.5e-3, 100)]:
+        G = adi.Patch(n, p, tau)
+        G.set_fields(f0)
+        G.step(st)
+        runs.append(G.get_fields())
+    for grp in (slice(0, 3), slice(3, 6)):
+        d1 = np.sqrt(sum(np.sum((a - b) ** 2) for a, b in zip(runs[0][grp], runs[1][grp])))
+        d2 = np.sqrt(sum(np.sum((a - b) ** 2) for a, b in zip(runs[1][grp], runs[2][grp])))
+        order = math.log2(d1 / d2)
+        assert 1.8 <= order <= 2.2, order
