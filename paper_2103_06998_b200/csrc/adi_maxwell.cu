@@ -333,9 +333,11 @@ adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp
   }
   args.kchunk = rhs_kchunk(P, args.nzout);
   args.tab = P->d_tab;
-  args.a = P->a;
-  args.b = P->b;
-  args.c = P->c;
+  if (!args.a && !args.b && !args.c) {  // the patch's row factors (box calls bring their own)
+    args.a = P->a;
+    args.b = P->b;
+    args.c = P->c;
+  }
   args.step = P->d_step;
   for (int ax = 0; ax < 3; ax++) active_range(P, comp, ax, args.lo[ax], args.hi[ax]);
   // interior Toeplitz rows (row N/2 of M, A, B; identical for rows 2P..N-2P-1)
@@ -1610,12 +1612,10 @@ adi_status adi_box_rhs(adi_patch P, int32_t kind, int32_t s, int32_t d, const do
   args.use_sdirect = 1;
   args.sdirect = sval;
   args.out = out;
-  // launch_rhs takes the row factors from the patch: point them at the caller's box arrays
-  double *pa = P->a, *pb = P->b, *pc = P->c;
-  P->a = const_cast<double*>(a), P->b = const_cast<double*>(b), P->c = const_cast<double*>(c);
-  adi_status st = launch_rhs(P, args, kind, s, kind == 0 ? d : 3 + d, kind == 0 ? ADI_K_RHS_E : ADI_K_RHS_H);
-  P->a = pa, P->b = pb, P->c = pc;
-  return poison(P, st);
+  args.a = a;  // the caller's box-layout row factors
+  args.b = b;
+  args.c = c;
+  return poison(P, launch_rhs(P, args, kind, s, kind == 0 ? d : 3 + d, kind == 0 ? ADI_K_RHS_E : ADI_K_RHS_H));
 }
 
 adi_status adi_box_copy(adi_patch P, double* dst, const int64_t ddims[3], const int64_t doff[3], const double* src,
