@@ -416,3 +416,34 @@ def test_c2_full_config_parity_and_temporal_order():
         d2 = np.sqrt(sum(np.sum((a - b) ** 2) for a, b in zip(runs[1][grp], runs[2][grp])))
         order = math.log2(d1 / d2)
         assert 1.8 <= order <= 2.2, order
+
+
+@pytest.mark.parametrize("tau_key,l2_key,hc_key,tau", [
+    ("tau_1_10", "l2_bound_tau_1_10", "hcurl_bound_tau_1_10", 1.0 / 10),
+    ("tau_1_1280", "l2_bound_tau_1_1280", "hcurl_bound_tau_1_1280", 1.0 / 1280)])
+def test_exp1_paper_bounds_on_gpu(tau_key, l2_key, hc_key, tau):
+    """EXP-1 on the device: the manufactured solution u_A on 16^3
+    elements (p = 2) stepped by the GPU to T = 1; the L2 and H(curl) errors of E and H
+    (max over sampled times, evaluated from the GPU's coefficients by the oracle's Gauss
+    quadrature, q = p+3) stay below the bounds PAPER.md prints (P:320-321,
+    tests/golden/paper_values.txt)."""
+    from tests.test_oracle_pins import golden_values
+
+    gv = golden_values()
+    n, p = int(gv["mesh_elements_per_axis"]), 2
+    steps = int(round(1.0 / tau))
+    O = oracle.Patch(n, p, tau)
+    O.project_uA(0.0)
+    G = adi.Patch(n, p, tau)
+    G.set_fields(O.get_fields())
+    chunk = max(1, steps // 10)
+    mx = np.zeros(4)
+    done = 0
+    while done < steps:
+        k = min(chunk, steps - done)
+        G.step(k)
+        done += k
+        O.set_fields(G.get_fields())
+        mx = np.maximum(mx, O.errors_uA(done * tau))
+    assert mx[0] < gv[l2_key] and mx[1] < gv[l2_key], mx
+    assert mx[2] < gv[hc_key] and mx[3] < gv[hc_key], mx
