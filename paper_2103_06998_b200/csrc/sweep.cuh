@@ -45,6 +45,12 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #define ADI_SW_CH_DER 8
 #define ADI_SW_RS_DER 4
 #endif
+// Row-modified sweep: recompute the pivots 1/u_kk in the recurrence (1) instead of
+// streaming the cached pivot array (0).  The cache is still built (and gated, D12) at
+// set_materials; the recomputation is the same arithmetic, so results are bit-identical.
+#ifndef ADI_SW_MOD_RECIP
+#define ADI_SW_MOD_RECIP 1
+#endif
 #ifndef ADI_SW_MINB_MASS  // resident blocks the mass kernel's register budget is sized for
 #define ADI_SW_MINB_MASS 2
 #endif
@@ -53,12 +59,14 @@ constexpr int SW_CH_MOD = ADI_SW_CH_MOD, SW_RS_MOD = ADI_SW_RS_MOD;
 constexpr int SW_CH_DER = ADI_SW_CH_DER, SW_RS_DER = ADI_SW_RS_DER;
 __host__ __device__ constexpr int sw_ch(int mode) { return mode == SW_MOD ? SW_CH_MOD : mode == SW_DER ? SW_CH_DER : SW_CH_MASS; }
 __host__ __device__ constexpr int sw_rs(int mode) { return mode == SW_MOD ? SW_RS_MOD : mode == SW_DER ? SW_RS_DER : SW_RS_MASS; }
-__host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? 3 : mode == SW_DER ? 2 : 1; }
+constexpr bool SW_MOD_RECIP = ADI_SW_MOD_RECIP != 0;
+__host__ __device__ constexpr int sw_na(int mode) { return mode == SW_MOD ? (SW_MOD_RECIP ? 2 : 3) : mode == SW_DER ? 2 : 1; }
 // checkpoint words per chunk: y window (P); MOD adds the U entries u_{k-m,k-m+j}, j < P
-// (P(P-1); the pivots and u_{k-m,k-m+P} = M + c S entries are re-read from the pivot
-// cache and c); DER: y only (the u window is re-read from u)
+// (P(P-1); u_{k-m,k-m+P} = M + c S entries are re-read from c, the pivots 1/u_{k-m,k-m}
+// from the pivot cache or, with SW_MOD_RECIP, kept in the checkpoint: P more words);
+// DER: y only (the u window is re-read from u)
 __host__ __device__ constexpr int sw_state_words(int mode, int P) {
-  return mode == SW_MOD ? P * P : P;
+  return mode == SW_MOD ? P * P + (SW_MOD_RECIP ? P : 0) : P;
 }
 // (the twisted kernel keeps the u window in its checkpoints)
 __host__ __device__ constexpr int sw_state_words_tw(int mode, int P) { return mode == SW_DER ? 2 * P : P; }
@@ -125,6 +133,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
   constexpr int SLOT = NA * CH * 33;
   constexpr int SWD = sw_state_words(MODE, P);
   constexpr int UW = MOD && P > 1 ? P - 1 : 1;  // stash width of U entries per row (pass 2)
+  constexpr bool RECIP = MOD && SW_MOD_RECIP;     // pivots recomputed, not streamed
   static_assert(!DER || (RS >= 3 && CH >= P), "derivative mode needs the next chunk resident");
   extern __shared__ double sw_smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
                                                                        : (int64_t)J.dims[0] * J.dims[1];
       src[0] = J.in;
       src[1] = DER ? J.base : J.c;
-      src[2] = J.iu;
+      src[2] = RECIP ? nullptr : J.iu;
       out = J.out;
       coef = J.coef;
       axis = J.axis;
@@ -290,7 +299,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       return fv;
     };
     // one forward elimination step (row k): returns y_k, and (MOD) u_{k,k+q}, q = 1..P in un[]
-    auto fwd = [&](auto fast, int row, double fv, double cc, double ivk, double* un) -> double {
+    auto fwd = [&](auto fast, int row, double fv, double cc, double ivk, double* un, double& ivo) -> double {
       double y = fv;
       if (MOD) {
         double a[W];
@@ -304,6 +313,13 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
           for (int mp = P; mp > m; mp--) s = fma(-l[mp], uw[mp - 1][mp - m - 1], s);
           l[m] = s * iw[m - 1];
         }
+        if (RECIP) {  // u_kk exactly as factor_kernel forms it
+          double u0 = a[P];
+#pragma unroll
+          for (int m = 1; m <= P; m++) u0 = fma(-l[m], uw[m - 1][m - 1], u0);
+          ivk = 1.0 / u0;
+        }
+        ivo = ivk;
 #pragma unroll
         for (int q = 1; q <= P; q++) {
           double s = a[P + q];
@@ -341,6 +357,10 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
 #pragma unroll
           for (int j = 0; j < P - 1; j++) p[(P + m * (P - 1) + j) * 32] = uw[m][j];
       }
+      if (RECIP) {
+#pragma unroll
+        for (int m = 0; m < P; m++) p[(P * P + m) * 32] = iw[m];
+      }
     };
     // pv[m-1], pc[m-1]: pivot 1/u and c of patch row r0 - m (MOD; loaded ahead of time)
     auto set_state = [&](const double* p, const double* pv, const double* pc, int r0) {
@@ -352,7 +372,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
 #pragma unroll
           for (int j = 0; j < P - 1; j++) uw[m][j] = p[P + m * (P - 1) + j];
           const int row = r0 - 1 - m;
-          iw[m] = row >= lo ? pv[m] : 0.0;
+          iw[m] = row >= lo ? (RECIP ? p[P * P + m] : pv[m]) : 0.0;
           uw[m][P - 1] = row >= lo ? mod_entry(std::false_type{}, row, pc[m], 2 * P) : 0.0;
         }
       }
@@ -377,7 +397,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
     // (and u_{r0+CH-P..r0+CH+P-1} on exit).
     double xw[P];
     auto fwd_chunk = [&](auto fast, const double* sl, const double* nx, const double* hd, int r0, double* y,
-                         double* us) {
+                         double* us, double* ivs) {
 #pragma unroll
       for (int r = 0; r < CH; r++) {
         const int row = r0 + r;
@@ -393,9 +413,11 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
           } else {
             fv = sl[r * 33 + lane];
           }
+          double ivo;
           const double yy = fwd(fast, row, fv, MOD ? sl[(CH + r) * 33 + lane] : 0.0,
-                                MOD ? sl[(2 * CH + r) * 33 + lane] : 0.0, un);
+                                MOD && !RECIP ? sl[(2 * CH + r) * 33 + lane] : 0.0, un, ivo);
           if (y) y[r] = yy;
+          if (RECIP && ivs) ivs[r] = ivo;
           if (MOD && us) {
 #pragma unroll
             for (int q = 0; q < P - 1; q++) us[r * UW + q] = un[q];
@@ -404,7 +426,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       }
     };
     // back substitution of one chunk (y[] -> x[] in place)
-    auto bwd_chunk = [&](auto fast, const double* sl, int r0, double* y, double* us) {
+    auto bwd_chunk = [&](auto fast, const double* sl, int r0, double* y, double* us, const double* ivs) {
 #pragma unroll
       for (int r = CH - 1; r >= 0; r--) {
         const int row = r0 + r;
@@ -415,7 +437,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
             x = fma(-mod_entry(fast, row, cc, 2 * P), xw[P - 1], x);
 #pragma unroll
             for (int q = P - 1; q >= 1; q--) x = fma(-us[r * UW + q - 1], xw[q - 1], x);
-            x *= sl[(2 * CH + r) * 33 + lane];
+            x *= RECIP ? ivs[r] : sl[(2 * CH + r) * 33 + lane];
           } else {
 #pragma unroll
             for (int q = P - 1; q >= 0; q--) x = fma(-fac_entry(fast, row, P + 1 + q), xw[q], x);
@@ -506,9 +528,9 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
         double yv[P + CH];
         fwd_fast_cm(sl, nx, nullptr, yv);
       } else if (chunk_fast(r0)) {
-        fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+        fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr, nullptr);
       } else {
-        fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr);
+        fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr, nullptr);
       }
       __syncwarp();
       if (c + RS - 1 < nc) issue(c + RS - 1, 1);
@@ -533,7 +555,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
         for (int m = 0; m < P; m++) {
           const int row = max(r0 - 1 - m, lo);
           if (MOD) {
-            pv[m] = __ldg(src[2] + base + (int64_t)row * stride);
+            if (!RECIP) pv[m] = __ldg(src[2] + base + (int64_t)row * stride);
             pc[m] = __ldg(src[1] + base + (int64_t)row * stride);
           } else {
             pv[m] = __ldg(src[0] + base + (int64_t)row * stride);
@@ -561,18 +583,19 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       if (DER) der_prime(sl, r0);
       double y[CH];
       double us[CH * UW];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
+      double ivs[RECIP ? CH : 1];  // recomputed pivots 1/u_kk of the chunk
       if (!MOD && chunk_fast(r0)) {
         double yv[P + CH];
         fwd_fast_cm(sl, nullptr, hd, yv);
         bwd_fast_cm(yv, y);
       } else if (chunk_fast(r0)) {
-        fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us);
-        bwd_chunk(std::true_type{}, sl, r0, y, us);
+        fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us, ivs);
+        bwd_chunk(std::true_type{}, sl, r0, y, us, ivs);
       } else {
 #pragma unroll
         for (int r = 0; r < CH; r++) y[r] = 0.0;
-        fwd_chunk(std::false_type{}, sl, nullptr, hd, r0, y, us);
-        bwd_chunk(std::false_type{}, sl, r0, y, us);
+        fwd_chunk(std::false_type{}, sl, nullptr, hd, r0, y, us, ivs);
+        bwd_chunk(std::false_type{}, sl, r0, y, us, ivs);
       }
       if (DER) {
 #pragma unroll
