@@ -355,15 +355,13 @@ adi_status launch_rhs(adi_patch P, adi::RhsArgs& args, int kind, int s, int comp
   const int nt = kind == 0 ? 4 : 3;
   for (int t = 0; t < nt && tma; t++) tma = make_field_map(&maps.m[t], args.u[t], N, args.nzin, P->p);
   const int nch = (args.nzout + args.kchunk - 1) / args.kchunk;
-  // interior tiles (every output row Toeplitz in x and y): tiles 1 .. (N-2p)/T - 1 -> FAST launch;
-  // the rim tiles -> the general launch (compact grid)
+  // interior tiles (every output row Toeplitz in x and y): tiles 1 .. (N-2p)/T - 1 (FAST
+  // code path); the rim tiles take the general path; one launch, rim tiles first per z-chunk
   const int ntx = (N + adi::RX_TX - 1) / adi::RX_TX, nty = (N + adi::RX_TY - 1) / adi::RX_TY;
   const int fx = std::max(0, (N - 2 * P->p) / adi::RX_TX - 1), fy = std::max(0, (N - 2 * P->p) / adi::RX_TY - 1);
   args.ntx = ntx, args.nty = nty, args.fx = fx && fy ? fx : 0, args.fy = fx && fy ? fy : 0;
-  dim3 grid(ntx * nty - args.fx * args.fy, 1, nch);
-  dim3 gfast(args.fx, args.fy, args.fx ? nch : 0);
-  if (fx && fy) P->launch_counter++;  // the interior-tile launch is a second kernel
-  with_degree(P->p, [&](auto ops) { ops.rhs(P->stream, grid, gfast, args, maps, tma, kind, s, d); });
+  dim3 grid(ntx * nty, 1, nch);
+  with_degree(P->p, [&](auto ops) { ops.rhs(P->stream, grid, args, maps, tma, kind, s, d); });
   CUDA_TRY(cudaGetLastError());
   return ADI_OK;
 }

@@ -11,15 +11,10 @@ namespace adi {
 namespace {
 template <int KIND, int S, int D>
 struct RhsF {
-  static void run(cudaStream_t st, dim3 g, dim3 gf, const RhsArgs& a, const RhsMaps& m, bool tma) {
+  static void run(cudaStream_t st, dim3 g, const RhsArgs& a, const RhsMaps& m, bool tma) {
     constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
-    if (tma) {
-      if (gf.x * gf.y) rhs_kernel<ADI_P, KIND, S, D, true, true><<<gf, RX_THREADS, smem, st>>>(m, a);
-      rhs_kernel<ADI_P, KIND, S, D, true, false><<<g, RX_THREADS, smem, st>>>(m, a);
-    } else {
-      if (gf.x * gf.y) rhs_kernel<ADI_P, KIND, S, D, false, true><<<gf, RX_THREADS, smem, st>>>(m, a);
-      rhs_kernel<ADI_P, KIND, S, D, false, false><<<g, RX_THREADS, smem, st>>>(m, a);
-    }
+    if (tma) rhs_kernel<ADI_P, KIND, S, D, true><<<g, RX_THREADS, smem, st>>>(m, a);
+    else rhs_kernel<ADI_P, KIND, S, D, false><<<g, RX_THREADS, smem, st>>>(m, a);
   }
 };
 template <int KIND, int S, int D>
@@ -27,29 +22,27 @@ cudaError_t rhs_attr_one() {
   constexpr size_t smem = rhs_smem_bytes<ADI_P, RhsProg<KIND, S, D>::NT>();
   const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true, true>, A, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true, false>, A, (int)smem))) return e;
-  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false, true>, A, (int)smem))) return e;
-  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false, false>, A, (int)smem);
+  if ((e = cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, true>, A, (int)smem))) return e;
+  return cudaFuncSetAttribute(rhs_kernel<ADI_P, KIND, S, D, false>, A, (int)smem);
 }
 }  // namespace
 
 template <>
-void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, dim3 gfast, const RhsArgs& args, const RhsMaps& maps, bool tma,
+void Ops<ADI_P>::rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma,
                      int kind, int s, int d) {
   switch (kind * 6 + (s - 1) * 3 + d) {
-    case 0: RhsF<0, 1, 0>::run(st, grid, gfast, args, maps, tma); break;
-    case 1: RhsF<0, 1, 1>::run(st, grid, gfast, args, maps, tma); break;
-    case 2: RhsF<0, 1, 2>::run(st, grid, gfast, args, maps, tma); break;
-    case 3: RhsF<0, 2, 0>::run(st, grid, gfast, args, maps, tma); break;
-    case 4: RhsF<0, 2, 1>::run(st, grid, gfast, args, maps, tma); break;
-    case 5: RhsF<0, 2, 2>::run(st, grid, gfast, args, maps, tma); break;
-    case 6: RhsF<1, 1, 0>::run(st, grid, gfast, args, maps, tma); break;
-    case 7: RhsF<1, 1, 1>::run(st, grid, gfast, args, maps, tma); break;
-    case 8: RhsF<1, 1, 2>::run(st, grid, gfast, args, maps, tma); break;
-    case 9: RhsF<1, 2, 0>::run(st, grid, gfast, args, maps, tma); break;
-    case 10: RhsF<1, 2, 1>::run(st, grid, gfast, args, maps, tma); break;
-    default: RhsF<1, 2, 2>::run(st, grid, gfast, args, maps, tma); break;
+    case 0: RhsF<0, 1, 0>::run(st, grid, args, maps, tma); break;
+    case 1: RhsF<0, 1, 1>::run(st, grid, args, maps, tma); break;
+    case 2: RhsF<0, 1, 2>::run(st, grid, args, maps, tma); break;
+    case 3: RhsF<0, 2, 0>::run(st, grid, args, maps, tma); break;
+    case 4: RhsF<0, 2, 1>::run(st, grid, args, maps, tma); break;
+    case 5: RhsF<0, 2, 2>::run(st, grid, args, maps, tma); break;
+    case 6: RhsF<1, 1, 0>::run(st, grid, args, maps, tma); break;
+    case 7: RhsF<1, 1, 1>::run(st, grid, args, maps, tma); break;
+    case 8: RhsF<1, 1, 2>::run(st, grid, args, maps, tma); break;
+    case 9: RhsF<1, 2, 0>::run(st, grid, args, maps, tma); break;
+    case 10: RhsF<1, 2, 1>::run(st, grid, args, maps, tma); break;
+    default: RhsF<1, 2, 2>::run(st, grid, args, maps, tma); break;
   }
 }
 

@@ -17,8 +17,8 @@ template <int P>
 struct Ops {
   // RHS of the E (kind 0) / H (kind 1) system of component d in substep s.
   // tma: halo planes by cp.async.bulk.tensor (maps valid), else cp.async.
-  // gfast: grid of the interior-tile launch (may be empty); grid: all tiles.
-  static void rhs(cudaStream_t st, dim3 grid, dim3 gfast, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind,
+  // grid: (every tile, 1, z-chunks); one launch (rim tiles first, then the interior ones).
+  static void rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind,
                   int s, int d);
   static cudaError_t rhs_attrs();
   // One batched sweep launch (persistent grid chosen by the caller).

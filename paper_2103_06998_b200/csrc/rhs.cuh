@@ -144,14 +144,13 @@ __device__ __forceinline__ void rx_wait() { asm volatile("cp.async.wait_group %0
 
 // out[I] = sum_t sign_t * scale_t[I] * ((X_t (x) Y_t (x) Z_t) u_t)[I]  (- a s J),
 // zero outside the active set.
-// FAST: the tile is interior in x and y (every output row Toeplitz): x/y
-// coefficients come from the parameter bank; the general variant reads them
-// from per-block shared tables (rows of the band tables) and returns at once
-// for interior tiles (they are covered by the FAST launch).  z coefficients
-// always come from a per-block shared table (uniform broadcast reads).
+// One (x,y) tile, z-chunk blockIdx.z.  FAST: the tile is interior in x and y (every
+// output row Toeplitz): x/y coefficients come from the parameter bank; the general
+// variant (rim tiles) reads them from per-block shared tables (rows of the band
+// tables).  z coefficients always come from a per-block shared table (uniform
+// broadcast reads).  bid: the tile's index among the interior / rim tiles.
 template <int P, int KIND, int S, int D, bool TMA, bool FAST>
-__global__ void __launch_bounds__(RX_THREADS, 2)
-rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs args) {
+__device__ __forceinline__ void rhs_tile(const RhsMaps& maps, const RhsArgs& args, const int bid) {
   using Prog = RhsProg<KIND, S, D>;
   using G = RxGeom<P>;
   constexpr int NT = Prog::NT;
@@ -171,10 +170,11 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
   // full rows {0} u [fy+1, nty) followed by the side tiles {0} u [fx+1, ntx) of rows [1, fy]
   int bx, by;
   if (FAST) {
-    bx = blockIdx.x + 1;
-    by = blockIdx.y + 1;
+    by = bid / args.fx;
+    bx = bid - by * args.fx + 1;
+    by += 1;
   } else {
-    const int e = blockIdx.x, nfull = (args.nty - args.fy) * args.ntx;
+    const int e = bid, nfull = (args.nty - args.fy) * args.ntx;
     if (e < nfull) {
       const int ri = e / args.ntx;
       bx = e - ri * args.ntx;
@@ -403,6 +403,18 @@ rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs
     }
   }
   if (!TMA) rx_wait<0>();
+}
+
+// One launch covers every tile: in each z-chunk the rim tiles come first (they
+// are slower: shared-table stencils, ragged tails), then the interior tiles, so
+// the rim overlaps the interior work instead of forming a launch of its own.
+template <int P, int KIND, int S, int D, bool TMA>
+__global__ void __launch_bounds__(RX_THREADS, 2)
+rhs_kernel(const __grid_constant__ RhsMaps maps, const __grid_constant__ RhsArgs args) {
+  const int nrim = args.ntx * args.nty - args.fx * args.fy;
+  const int b = blockIdx.x;
+  if (b < nrim) rhs_tile<P, KIND, S, D, TMA, false>(maps, args, b);
+  else rhs_tile<P, KIND, S, D, TMA, true>(maps, args, b - nrim);
 }
 
 }  // namespace adi

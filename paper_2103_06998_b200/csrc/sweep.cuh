@@ -41,7 +41,7 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #define ADI_SW_CH_MASS 16
 #define ADI_SW_RS_MASS 4
 #define ADI_SW_CH_MOD 8
-#define ADI_SW_RS_MOD 5
+#define ADI_SW_RS_MOD 3
 #define ADI_SW_CH_DER 8
 #define ADI_SW_RS_DER 4
 #endif
@@ -53,6 +53,9 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #endif
 #ifndef ADI_SW_MINB_MASS  // resident blocks the mass kernel's register budget is sized for
 #define ADI_SW_MINB_MASS 2
+#endif
+#ifndef ADI_SW_MINB_MOD
+#define ADI_SW_MINB_MOD 1
 #endif
 constexpr int SW_CH_MASS = ADI_SW_CH_MASS, SW_RS_MASS = ADI_SW_RS_MASS;
 constexpr int SW_CH_MOD = ADI_SW_CH_MOD, SW_RS_MOD = ADI_SW_RS_MOD;
@@ -126,7 +129,7 @@ template <int N>
 __device__ __forceinline__ void sw_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int P, int MODE>
-__global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_MASS : 1) sweep_kernel(const __grid_constant__ SweepBatch B) {
+__global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_MASS : MODE == SW_MOD ? ADI_SW_MINB_MOD : 1) sweep_kernel(const __grid_constant__ SweepBatch B) {
   constexpr bool MOD = MODE == SW_MOD, DER = MODE == SW_DER;
   constexpr int CH = sw_ch(MODE), RS = sw_rs(MODE), NA = sw_na(MODE);
   constexpr int W = 2 * P + 1;
