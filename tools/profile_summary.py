@@ -71,15 +71,17 @@ def main(tag, cfg):
         mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         b = sum(float(r[ix[k]].replace(",", "")) * mul.get(ru[ix[k]], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         traffic.setdefault(kclass(name), []).append(b)
-    # rhs_e: bytes per component = interior-tile + boundary-tile launch
+    # one launch per RHS component (rounds before r1e: interior-tile + boundary-tile
+    # launches, captured as two kernels of the same class; pass --split-rhs for those)
+    split = "--split-rhs" in sys.argv
     bpl = {}
     for c, v in traffic.items():
-        bpl[c] = sum(v) / (len(v) / 2 if c in ("rhs_e", "rhs_h") else len(v))
+        bpl[c] = sum(v) / (len(v) / 2 if split and c in ("rhs_e", "rhs_h") else len(v))
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     open(os.path.join(ROOT, "profiles", f"ncu_{cfg}_{tag}.md"), "w").write("\n".join(out) + "\n")
     json.dump({"config": cfg, "tag": tag, "bytes_per_launch": bpl,
                "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from one ncu --set full capture "
-                       "(rhs_e/rhs_h: per component = interior-tile + boundary-tile launch)"},
+                       "(rhs_e/rhs_h: one launch per component)"},
               open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     print("\n".join(out))
     print(bpl)
