@@ -131,6 +131,18 @@ adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
  * (conserved by the curl part of the scheme).  Synchronises.  Whole patches only. */
 adi_status adi_energy(adi_patch patch, double out[7]);
 
+/* Second workload: the test-function-weighted L2 projection of the
+ * Appendix, in 3D: solve K u = f with K = diag(eps^) (M (x) M (x) M), i.e. row i
+ * of the Kronecker mass matrix scaled by eps^_i (the coefficient carries the index of the test
+ * function).  The Appendix's block splitting (eqs. split1, split2) gives
+ * u = (M^-1 (x) M^-1 (x) M^-1)(f / eps^): one division pass and three mass sweeps, O(N^3).
+ * f, eps_tf, u: DEVICE pointers to N^3 doubles (x fastest), owned by the caller; u may equal f.
+ * Full index range along every axis (no PEC elimination).  Runs on the patch's stream
+ * (asynchronous except for the eps check, which synchronises).  ADI_ERR_ARG for NULL pointers
+ * or an eps^ entry that is not finite and > 0 (u untouched); ADI_ERR_STATE for a box-mode
+ * patch.  Whole patches only. */
+adi_status adi_project_weighted(adi_patch patch, const double* f, const double* eps_tf, double* u);
+
 /* Block until all work queued on the patch stream has finished. */
 adi_status adi_synchronize(adi_patch patch);
 

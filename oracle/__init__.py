@@ -56,6 +56,7 @@ def lib():
             L.orc_exact_uA.argtypes = [C.c_double, C.c_double, C.c_double, C.c_double, _dp, _dp]
             L.orc_errors_uA.argtypes = [C.c_void_p, C.c_double, _dp]
             L.orc_project_uA.argtypes = [C.c_void_p, C.c_double]
+            L.orc_project_weighted.argtypes = [C.c_void_p, _dp, _dp, _dp]
             L.orc_point_load.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, _dp]
             L.orc_set_source.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_int64]
             _lib = L
@@ -221,6 +222,14 @@ class Patch:
     # -- manufactured solution --------------------------------------------------
     def project_uA(self, t: float = 0.0):
         self._check(self._L.orc_project_uA(self.h, float(t)))
+
+    def project_weighted(self, f, eps_tf):
+        """NEXT-4 (Appendix, P:680-830): u with diag(eps)(M (x) M (x) M) u = f."""
+        ff = np.ascontiguousarray(f, dtype=np.float64).reshape(-1)
+        ee = np.ascontiguousarray(eps_tf, dtype=np.float64).reshape(-1)
+        u = np.zeros(self.U)
+        self._check(self._L.orc_project_weighted(self.h, _ptr(ff), _ptr(ee), _ptr(u)))
+        return u
 
     def errors_uA(self, t: float):
         out = np.zeros(4)

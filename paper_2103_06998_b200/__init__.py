@@ -39,7 +39,7 @@ EXPORTS = [
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
-    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy",
+    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted",
 ]
 
 
@@ -144,6 +144,7 @@ def lib():
             L.adi_box_materials_tf.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.adi_set_sweep_order.argtypes = [C.c_void_p, C.c_int32]
             L.adi_energy.argtypes = [C.c_void_p, C.c_void_p]
+            L.adi_project_weighted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             _lib = L
         return _lib
 
@@ -269,6 +270,18 @@ class Patch:
         out = (C.c_double * 7)()
         self._check(self._L.adi_energy(self.h, out))
         return [out[c] for c in range(6)], out[6]
+
+    def project_weighted(self, f, eps_tf, out=None):
+        """NEXT-4 (Appendix, P:680-830): u with diag(eps^)(M (x) M (x) M) u = f.  f, eps_tf: CUDA
+        float64 tensors of N^3 entries (x fastest); out (default: a new tensor) may be f.
+        Asynchronous on the patch stream."""
+        import torch
+        if out is None:
+            out = torch.empty_like(f)
+        for t in (f, eps_tf, out):
+            assert t.is_cuda and t.numel() == self.N ** 3, "need CUDA tensors of N^3 entries"
+        self._check(self._L.adi_project_weighted(self.h, _addr(f), _addr(eps_tf), _addr(out)))
+        return out
 
     def set_timing(self, enable: bool):
         self._check(self._L.adi_set_timing(self.h, int(bool(enable))))

@@ -1711,4 +1711,33 @@ adi_status adi_energy(adi_patch P, double out[7]) {
   return ADI_OK;
 }
 
+// Appendix: K u = f with K = diag(eps^) (M (x) M (x) M), the test-function-weighted
+// L2 projection.  Splitting the blocks as the Appendix does (eq. split1: A_j = diag(eps_.j) M,
+// G_j = A_j^{-1} F_j = M^{-1} diag(1/eps_.j) F_j; eq. split2: the remaining Kronecker mass
+// systems), u = (M^{-1} (x) M^{-1} (x) M^{-1}) (f / eps^): one division pass and three mass
+// sweeps on the full index range (no boundary rows eliminated).
+adi_status adi_project_weighted(adi_patch P, const double* f, const double* eps_tf, double* u) {
+  CHECK_PATCH(P);
+  if (P->cfg.nranks != 1)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_project_weighted needs the whole patch");
+  if (!f || !eps_tf || !u) return fail(ADI_ERR_ARG, "adi_project_weighted: NULL pointer");
+  adi_status st = check_positive(P, eps_tf, P->U, "eps");
+  if (st) return st;
+  {
+    LaunchScope ls(P, ADI_K_OTHER);
+    adi::div_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(u, f, eps_tf, P->U);
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int ax = 0; ax < 3; ax++) {
+    SweepReq r{};
+    r.comp = 3 + ax;  // an H component: active range [0, N) along every axis under both BCs
+    r.axis = ax;
+    r.in = u;
+    r.out = u;
+    r.iu = nullptr;
+    if ((st = launch_sweeps(P, &r, 1, adi::SW_MASS))) return st;
+  }
+  return ADI_OK;
+}
+
 }  // extern "C"

@@ -64,6 +64,12 @@ __global__ void pec_zero_kernel(double* __restrict__ u, int N, int lo0, int hi0,
 
 __global__ void increment_kernel(int64_t* counter) { *counter += 1; }
 
+// u = f / eps (first step of the eps-weighted projection, Appendix eq. split1); u may alias f
+__global__ void div_kernel(double* u, const double* f, const double* __restrict__ eps, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    u[i] = f[i] / eps[i];
+}
+
 __global__ void fill_kernel(double* __restrict__ x, int64_t n, double v) {
   for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) x[I] = v;
 }
