@@ -131,6 +131,14 @@ adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
  * (conserved by the curl part of the scheme).  Synchronises.  Whole patches only. */
 adi_status adi_energy(adi_patch patch, double out[7]);
 
+/* On-device diagnostic: errors of the current fields against the
+ * manufactured solution u_A(., t) (sign reading D8; valid for eps = mu = 1):
+ * out[0] = ||E_h - E||_L2, out[1] = ||H_h - H||_L2, out[2] = ||E_h - E||_H(curl),
+ * out[3] = ||H_h - H||_H(curl) (H(curl)^2 = L2^2 + ||curl||^2, exact curl), by Gauss
+ * quadrature with q = p + 3 points per axis and element (D11).  Synchronises.  ADI_ERR_ARG
+ * for out == NULL; ADI_ERR_STATE for a box-mode patch.  Whole patches only. */
+adi_status adi_errors_uA(adi_patch patch, double t, double out[4]);
+
 /* Second workload: the test-function-weighted L2 projection of the
  * Appendix, in 3D: solve K u = f with K = diag(eps^) (M (x) M (x) M), i.e. row i
  * of the Kronecker mass matrix scaled by eps^_i (the coefficient carries the index of the test

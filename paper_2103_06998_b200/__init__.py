@@ -39,7 +39,7 @@ EXPORTS = [
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
-    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted",
+    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA",
 ]
 
 
@@ -145,6 +145,7 @@ def lib():
             L.adi_set_sweep_order.argtypes = [C.c_void_p, C.c_int32]
             L.adi_energy.argtypes = [C.c_void_p, C.c_void_p]
             L.adi_project_weighted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+            L.adi_errors_uA.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
             _lib = L
         return _lib
 
@@ -270,6 +271,12 @@ class Patch:
         out = (C.c_double * 7)()
         self._check(self._L.adi_energy(self.h, out))
         return [out[c] for c in range(6)], out[6]
+
+    def errors_uA(self, t: float):
+        """(||E_h-E||_L2, ||H_h-H||_L2, ||E_h-E||_Hcurl, ||H_h-H||_Hcurl) against u_A(., t)."""
+        out = (C.c_double * 4)()
+        self._check(self._L.adi_errors_uA(self.h, float(t), out))
+        return [out[k] for k in range(4)]
 
     def project_weighted(self, f, eps_tf, out=None):
         """NEXT-4 (Appendix, P:680-830): u with diag(eps^)(M (x) M (x) M) u = f.  f, eps_tf: CUDA

@@ -1711,6 +1711,62 @@ adi_status adi_energy(adi_patch P, double out[7]) {
   return ADI_OK;
 }
 
+// NEXT-3 on-device diagnostic: errors of the current fields against the manufactured solution
+// u_A(., t) (D8): out[0] = ||E_h - E||_L2, out[1] = ||H_h - H||_L2,
+// out[2] = ||E_h - E||_H(curl), out[3] = ||H_h - H||_H(curl), H(curl)^2 = L2^2 + ||curl||^2,
+// Gauss q = p + 3 per axis and element (D11).
+adi_status adi_errors_uA(adi_patch P, double t, double out[4]) {
+  CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_errors_uA needs the whole patch");
+  if (!out) return fail(ADI_ERR_ARG, "adi_errors_uA: out is NULL");
+  const int n = P->n, p = P->p, q = p + 3, pp = p + 1;
+  Space1D sp(n, p);
+  std::vector<double> gx, gw;
+  gauss01(q, gx, gw);
+  const double h = 1.0 / n;
+  std::vector<double> host((size_t)2 * n * q * pp + 2 * q), v(pp), d(pp);
+  double* bv = host.data();
+  double* bd = bv + (size_t)n * q * pp;
+  double* xg = bd + (size_t)n * q * pp;
+  double* wg = xg + q;
+  for (int e = 0; e < n; e++)
+    for (int g = 0; g < q; g++) {
+      sp.eval(sp.t[p + e] + h * gx[g], p + e, v.data(), d.data());  // B_{e..e+p} on element e
+      for (int j = 0; j < pp; j++) bv[((size_t)e * q + g) * pp + j] = v[j], bd[((size_t)e * q + g) * pp + j] = d[j];
+    }
+  for (int g = 0; g < q; g++) xg[g] = h * gx[g], wg[g] = h * gw[g];
+  double *dbuf, *acc;
+  const double** dF;
+  CUDA_TRY(cudaMallocAsync(&dbuf, host.size() * sizeof(double), P->stream));
+  CUDA_TRY(cudaMallocAsync(&acc, 4 * sizeof(double), P->stream));
+  CUDA_TRY(cudaMallocAsync(&dF, 6 * sizeof(double*), P->stream));
+  const double* hF[6];
+  for (int c = 0; c < 6; c++) hF[c] = P->F[c];
+  CUDA_TRY(cudaMemcpyAsync(dbuf, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(cudaMemcpyAsync(dF, hF, sizeof hF, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(cudaMemsetAsync(acc, 0, 4 * sizeof(double), P->stream));
+  {
+    LaunchScope ls(P, ADI_K_OTHER);
+    const double* dbv = dbuf;
+    adi::errors_uA_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(dF, n, p, q, dbv, dbv + (size_t)n * q * pp,
+                                                             dbv + (size_t)2 * n * q * pp,
+                                                             dbv + (size_t)2 * n * q * pp + q, h, t, acc);
+    CUDA_TRY(cudaGetLastError());
+  }
+  double hs[4];
+  CUDA_TRY(cudaMemcpyAsync(hs, acc, sizeof hs, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaFreeAsync(dbuf, P->stream));
+  CUDA_TRY(cudaFreeAsync(acc, P->stream));
+  CUDA_TRY(cudaFreeAsync(dF, P->stream));
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_errors_uA: %s", cudaGetErrorString(e)));
+  out[0] = std::sqrt(hs[0]);
+  out[1] = std::sqrt(hs[1]);
+  out[2] = std::sqrt(hs[0] + hs[2]);
+  out[3] = std::sqrt(hs[1] + hs[3]);
+  return ADI_OK;
+}
+
 // Appendix: K u = f with K = diag(eps^) (M (x) M (x) M), the test-function-weighted
 // L2 projection.  Splitting the blocks as the Appendix does (eq. split1: A_j = diag(eps_.j) M,
 // G_j = A_j^{-1} F_j = M^{-1} diag(1/eps_.j) F_j; eq. split2: the remaining Kronecker mass

@@ -70,6 +70,104 @@ __global__ void div_kernel(double* u, const double* f, const double* __restrict_
     u[i] = f[i] / eps[i];
 }
 
+// Manufactured solution u_A = g u^1_{1,1} + 2g u^2_{1,1} + 3g u^3_{1,1}, g = 2/sqrt(14)
+// (u^2 with the sign reading D8), and its curl (derived by hand):
+//   E = C (a1 sy sz, a2 sx sz, a3 sx sy),               C = cos(sqrt2 pi t), a_d = d g
+//   H = r S (sx (a2 cz - a3 cy), sy (a3 cx - a1 cz), sz (a1 cy - a2 cx)),  S = sin(sqrt2 pi t), r = 1/sqrt2
+//   curl E = pi C (sx (a3 cy - a2 cz), sy (a1 cz - a3 cx), sz (a2 cx - a1 cy))
+//   curl H = -2 pi r S (a1 sy sz, a2 sx sz, a3 sx sy)
+__device__ __forceinline__ void uA_field(double x, double y, double z, double t, double* f, double* cf) {
+  const double g = 2.0 / sqrt(14.0), a1 = g, a2 = 2.0 * g, a3 = 3.0 * g;
+  const double pi = 3.14159265358979323846, r = 0.70710678118654752440, om = 1.41421356237309504880 * pi;
+  double sx, cx, sy, cy, sz, cz, S, C;
+  sincos(pi * x, &sx, &cx);
+  sincos(pi * y, &sy, &cy);
+  sincos(pi * z, &sz, &cz);
+  sincos(om * t, &S, &C);
+  f[0] = C * a1 * sy * sz;
+  f[1] = C * a2 * sx * sz;
+  f[2] = C * a3 * sx * sy;
+  f[3] = r * S * sx * (a2 * cz - a3 * cy);
+  f[4] = r * S * sy * (a3 * cx - a1 * cz);
+  f[5] = r * S * sz * (a1 * cy - a2 * cx);
+  cf[0] = pi * C * sx * (a3 * cy - a2 * cz);
+  cf[1] = pi * C * sy * (a1 * cz - a3 * cx);
+  cf[2] = pi * C * sz * (a2 * cx - a1 * cy);
+  cf[3] = -2.0 * pi * r * S * a1 * sy * sz;
+  cf[4] = -2.0 * pi * r * S * a2 * sx * sz;
+  cf[5] = -2.0 * pi * r * S * a3 * sx * sy;
+}
+
+// Squared L2 errors of the discrete fields and of their curls against u_A(., t), by
+// Gauss quadrature with q points per axis on every element; one thread per (element,
+// Gauss point).  bv/bd[(e*q + g)*(p+1) + j]: B_{e+j} and B'_{e+j} at Gauss point g of
+// element e; x0/xg/wg: element starts (uniform h), points and weights on [0, h].
+// acc[0..3] += (E L2^2, H L2^2, curl E L2^2, curl H L2^2).
+__global__ void errors_uA_kernel(const double* const* __restrict__ F, int n, int p, int q,
+                                 const double* __restrict__ bv, const double* __restrict__ bd,
+                                 const double* __restrict__ xg, const double* __restrict__ wg, double h, double t,
+                                 double* acc) {
+  const int N = n + p, pp = p + 1;
+  const int64_t total = (int64_t)n * n * n * q * q * q;
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = id;
+    const int gi = (int)(r % q); r /= q;
+    const int gj = (int)(r % q); r /= q;
+    const int gk = (int)(r % q); r /= q;
+    const int ea = (int)(r % n); r /= n;
+    const int eb = (int)(r % n); r /= n;
+    const int ec = (int)r;
+    const double* vx = bv + ((int64_t)ea * q + gi) * pp;
+    const double* vy = bv + ((int64_t)eb * q + gj) * pp;
+    const double* vz = bv + ((int64_t)ec * q + gk) * pp;
+    const double* dx = bd + ((int64_t)ea * q + gi) * pp;
+    const double* dy = bd + ((int64_t)eb * q + gj) * pp;
+    const double* dz = bd + ((int64_t)ec * q + gk) * pp;
+    double val[6], gx[6], gy[6], gz[6];  // value and gradient of each discrete field
+    for (int c = 0; c < 6; c++) {
+      double v = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+      for (int kk = 0; kk < pp; kk++)
+        for (int jj = 0; jj < pp; jj++) {
+          const double* row = F[c] + (ea + (int64_t)N * ((eb + jj) + (int64_t)N * (ec + kk)));
+          const double yz = vy[jj] * vz[kk], dyz = dy[jj] * vz[kk], ydz = vy[jj] * dz[kk];
+          for (int ii = 0; ii < pp; ii++) {
+            const double u = row[ii];
+            v += u * vx[ii] * yz;
+            ax += u * dx[ii] * yz;
+            ay += u * vx[ii] * dyz;
+            az += u * vx[ii] * ydz;
+          }
+        }
+      val[c] = v, gx[c] = ax, gy[c] = ay, gz[c] = az;
+    }
+    const double cu[6] = {gy[2] - gz[1], gz[0] - gx[2], gx[1] - gy[0], gy[5] - gz[4], gz[3] - gx[5], gx[4] - gy[3]};
+    double ex[6], ecu[6];
+    uA_field(ea * h + xg[gi], eb * h + xg[gj], ec * h + xg[gk], t, ex, ecu);
+    const double w = wg[gi] * wg[gj] * wg[gk];
+    for (int c = 0; c < 3; c++) {
+      const double e0 = val[c] - ex[c], e1 = val[3 + c] - ex[3 + c], c0 = cu[c] - ecu[c], c1 = cu[3 + c] - ecu[3 + c];
+      s[0] += w * e0 * e0;
+      s[1] += w * e1 * e1;
+      s[2] += w * c0 * c0;
+      s[3] += w * c1 * c1;
+    }
+  }
+  __shared__ double red[4][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = 0; k < 4; k++) {
+    double v = s[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[k][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) v += red[threadIdx.x][w2];
+    atomicAdd(acc + threadIdx.x, v);
+  }
+}
+
 __global__ void fill_kernel(double* __restrict__ x, int64_t n, double v) {
   for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) x[I] = v;
 }

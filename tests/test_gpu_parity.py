@@ -444,6 +444,44 @@ def test_exp1_paper_bounds_on_gpu(tau_key, l2_key, hc_key, tau):
         G.step(k)
         done += k
         O.set_fields(G.get_fields())
-        mx = np.maximum(mx, O.errors_uA(done * tau))
+        oe = np.array(O.errors_uA(done * tau))
+        ge = np.array(G.errors_uA(done * tau))  # the same norms on the device (adi_errors_uA)
+        assert np.all(np.abs(ge - oe) <= 1e-9 * oe), (ge, oe)
+        mx = np.maximum(mx, oe)
     assert mx[0] < gv[l2_key] and mx[1] < gv[l2_key], mx
     assert mx[2] < gv[hc_key] and mx[3] < gv[hc_key], mx
+
+
+@pytest.mark.parametrize("n,p", [(5, 1), (9, 2), (6, 3), (4, 5)])
+def test_errors_uA_device_vs_oracle(n, p):
+    """NEXT-3: adi_errors_uA (device quadrature, q = p+3) equals the oracle's norms of the
+    same coefficients, at t = 0 (projection error only) and after steps."""
+    tau = 0.02
+    O = oracle.Patch(n, p, tau)
+    O.project_uA(0.0)
+    G = adi.Patch(n, p, tau)
+    G.set_fields(O.get_fields())
+    for steps in (0, 7):
+        G.step(steps)
+        t = G.step_index * tau
+        O.set_fields(G.get_fields())
+        oe, ge = np.array(O.errors_uA(t)), np.array(G.errors_uA(t))
+        assert np.all(np.abs(ge - oe) <= 1e-9 * oe), (steps, ge, oe)
+
+
+def test_exp1_temporal_order_device_norms_64():
+    """EXP-1 at 64^3 (beyond the oracle's stepping reach): u_A stepped by
+    the GPU to T = 0.5 at tau = 1/40 and 1/80; the device-evaluated L2 errors of E and H fall
+    by ~4x (second order in time), far above the spatial error at this mesh."""
+    n, p, T = 64, 2, 0.5
+    O = oracle.Patch(n, p, 0.1)
+    O.project_uA(0.0)
+    f0 = O.get_fields()
+    errs = []
+    for tau in (1 / 40, 1 / 80):
+        G = adi.Patch(n, p, tau)
+        G.set_fields(f0)
+        G.step(int(round(T / tau)))
+        errs.append(np.array(G.errors_uA(T)))
+    ratio = errs[0][:2] / errs[1][:2]
+    assert np.all((ratio > 3.3) & (ratio < 4.7)), (errs, ratio)
