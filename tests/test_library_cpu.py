@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "adi_maxwell.h")
 def declared_symbols():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(adi_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(adi_[A-Za-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
