@@ -139,6 +139,11 @@ adi_status adi_energy(adi_patch patch, double out[7]);
  * for out == NULL; ADI_ERR_STATE for a box-mode patch.  Whole patches only. */
 adi_status adi_errors_uA(adi_patch patch, double t, double out[4]);
 
+/* On-device diagnostic: out[0] = ||div E_h||_L2, out[1] = ||div H_h||_L2
+ * of the current fields, Gauss q = p + 3 per axis and element.  Synchronises.  ADI_ERR_ARG for
+ * out == NULL; ADI_ERR_STATE for a box-mode patch.  Whole patches only. */
+adi_status adi_divergence(adi_patch patch, double out[2]);
+
 /* Second workload: the test-function-weighted L2 projection of the
  * Appendix, in 3D: solve K u = f with K = diag(eps^) (M (x) M (x) M), i.e. row i
  * of the Kronecker mass matrix scaled by eps^_i (the coefficient carries the index of the test

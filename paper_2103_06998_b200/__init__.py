@@ -39,7 +39,7 @@ EXPORTS = [
     "adi_timing_report", "adi_debug_matrices", "adi_debug_materials_tf", "adi_debug_sweep", "adi_debug_rhs_e",
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
-    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA",
+    "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA", "adi_divergence",
 ]
 
 
@@ -146,6 +146,7 @@ def lib():
             L.adi_energy.argtypes = [C.c_void_p, C.c_void_p]
             L.adi_project_weighted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.adi_errors_uA.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
+            L.adi_divergence.argtypes = [C.c_void_p, C.c_void_p]
             _lib = L
         return _lib
 
@@ -277,6 +278,12 @@ class Patch:
         out = (C.c_double * 4)()
         self._check(self._L.adi_errors_uA(self.h, float(t), out))
         return [out[k] for k in range(4)]
+
+    def divergence(self):
+        """(||div E_h||_L2, ||div H_h||_L2) of the current fields."""
+        out = (C.c_double * 2)()
+        self._check(self._L.adi_divergence(self.h, out))
+        return [out[0], out[1]]
 
     def project_weighted(self, f, eps_tf, out=None):
         """NEXT-4 (Appendix, P:680-830): u with diag(eps^)(M (x) M (x) M) u = f.  f, eps_tf: CUDA

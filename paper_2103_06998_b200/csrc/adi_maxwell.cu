@@ -1711,15 +1711,11 @@ adi_status adi_energy(adi_patch P, double out[7]) {
   return ADI_OK;
 }
 
-// NEXT-3 on-device diagnostic: errors of the current fields against the manufactured solution
-// u_A(., t) (P:262-290, D8): out[0] = ||E_h - E||_L2, out[1] = ||H_h - H||_L2,
-// out[2] = ||E_h - E||_H(curl), out[3] = ||H_h - H||_H(curl), H(curl)^2 = L2^2 + ||curl||^2,
-// Gauss q = p + 3 per axis and element (D11).
-adi_status adi_errors_uA(adi_patch P, double t, double out[4]) {
-  CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_errors_uA needs the whole patch");
-  if (!out) return fail(ADI_ERR_ARG, "adi_errors_uA: out is NULL");
-  const int n = P->n, p = P->p, q = p + 3, pp = p + 1;
+// Gauss tables of the element-wise diagnostics: for every element e and Gauss point g (q per
+// axis, on [0, h]) the p+1 non-zero basis functions B_{e..e+p} (bv) and derivatives (bd), then
+// the points xg[q] and weights wg[q].  Layout: bv | bd | xg | wg.
+std::vector<double> quad_tables(adi_patch P, int q) {
+  const int n = P->n, p = P->p, pp = p + 1;
   Space1D sp(n, p);
   std::vector<double> gx, gw;
   gauss01(q, gx, gw);
@@ -1731,10 +1727,61 @@ adi_status adi_errors_uA(adi_patch P, double t, double out[4]) {
   double* wg = xg + q;
   for (int e = 0; e < n; e++)
     for (int g = 0; g < q; g++) {
-      sp.eval(sp.t[p + e] + h * gx[g], p + e, v.data(), d.data());  // B_{e..e+p} on element e
+      sp.eval(sp.t[p + e] + h * gx[g], p + e, v.data(), d.data());
       for (int j = 0; j < pp; j++) bv[((size_t)e * q + g) * pp + j] = v[j], bd[((size_t)e * q + g) * pp + j] = d[j];
     }
   for (int g = 0; g < q; g++) xg[g] = h * gx[g], wg[g] = h * gw[g];
+  return host;
+}
+
+// NEXT-3 on-device diagnostic: ||div E||_L2 and ||div H||_L2 of the current fields (Gauss
+// q = p + 3 per axis and element).
+adi_status adi_divergence(adi_patch P, double out[2]) {
+  CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_divergence needs the whole patch");
+  if (!out) return fail(ADI_ERR_ARG, "adi_divergence: out is NULL");
+  const int n = P->n, p = P->p, q = p + 3, pp = p + 1;
+  std::vector<double> host = quad_tables(P, q);
+  double *dbuf, *acc;
+  const double** dF;
+  CUDA_TRY(cudaMallocAsync(&dbuf, host.size() * sizeof(double), P->stream));
+  CUDA_TRY(cudaMallocAsync(&acc, 2 * sizeof(double), P->stream));
+  CUDA_TRY(cudaMallocAsync(&dF, 6 * sizeof(double*), P->stream));
+  const double* hF[6];
+  for (int c = 0; c < 6; c++) hF[c] = P->F[c];
+  CUDA_TRY(cudaMemcpyAsync(dbuf, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(cudaMemcpyAsync(dF, hF, sizeof hF, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(cudaMemsetAsync(acc, 0, 2 * sizeof(double), P->stream));
+  {
+    LaunchScope ls(P, ADI_K_OTHER);
+    const double* b = dbuf;
+    const size_t nt = (size_t)n * q * pp;
+    adi::divergence_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(dF, n, p, q, b, b + nt, b + 2 * nt + q, acc);
+    CUDA_TRY(cudaGetLastError());
+  }
+  double hs[2];
+  CUDA_TRY(cudaMemcpyAsync(hs, acc, sizeof hs, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(cudaFreeAsync(dbuf, P->stream));
+  CUDA_TRY(cudaFreeAsync(acc, P->stream));
+  CUDA_TRY(cudaFreeAsync(dF, P->stream));
+  cudaError_t e = cudaStreamSynchronize(P->stream);
+  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_divergence: %s", cudaGetErrorString(e)));
+  out[0] = std::sqrt(hs[0]);
+  out[1] = std::sqrt(hs[1]);
+  return ADI_OK;
+}
+
+// NEXT-3 on-device diagnostic: errors of the current fields against the manufactured solution
+// u_A(., t) (P:262-290, D8): out[0] = ||E_h - E||_L2, out[1] = ||H_h - H||_L2,
+// out[2] = ||E_h - E||_H(curl), out[3] = ||H_h - H||_H(curl), H(curl)^2 = L2^2 + ||curl||^2,
+// Gauss q = p + 3 per axis and element (D11).
+adi_status adi_errors_uA(adi_patch P, double t, double out[4]) {
+  CHECK_PATCH(P);
+  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): adi_errors_uA needs the whole patch");
+  if (!out) return fail(ADI_ERR_ARG, "adi_errors_uA: out is NULL");
+  const int n = P->n, p = P->p, q = p + 3, pp = p + 1;
+  const double h = 1.0 / n;
+  std::vector<double> host = quad_tables(P, q);
   double *dbuf, *acc;
   const double** dF;
   CUDA_TRY(cudaMallocAsync(&dbuf, host.size() * sizeof(double), P->stream));

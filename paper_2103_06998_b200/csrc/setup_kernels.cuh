@@ -168,6 +168,58 @@ __global__ void errors_uA_kernel(const double* const* __restrict__ F, int n, int
   }
 }
 
+// ||div E||^2 and ||div H||^2 of the discrete fields by Gauss quadrature (same tables and
+// thread mapping as errors_uA_kernel); acc[0..1] += (div E L2^2, div H L2^2).
+__global__ void divergence_kernel(const double* const* __restrict__ F, int n, int p, int q,
+                                  const double* __restrict__ bv, const double* __restrict__ bd,
+                                  const double* __restrict__ wg, double* acc) {
+  const int N = n + p, pp = p + 1;
+  const int64_t total = (int64_t)n * n * n * q * q * q;
+  double s[2] = {0.0, 0.0};
+  for (int64_t id = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; id < total; id += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = id;
+    const int gi = (int)(r % q); r /= q;
+    const int gj = (int)(r % q); r /= q;
+    const int gk = (int)(r % q); r /= q;
+    const int ea = (int)(r % n); r /= n;
+    const int eb = (int)(r % n); r /= n;
+    const int ec = (int)r;
+    const int64_t ox = ((int64_t)ea * q + gi) * pp, oy = ((int64_t)eb * q + gj) * pp, oz = ((int64_t)ec * q + gk) * pp;
+    double dv[2] = {0.0, 0.0};
+    for (int f = 0; f < 2; f++)        // E, H
+      for (int d = 0; d < 3; d++) {    // d/dx_d of component d
+        const double* X = d == 0 ? bd + ox : bv + ox;
+        const double* Y = d == 1 ? bd + oy : bv + oy;
+        const double* Z = d == 2 ? bd + oz : bv + oz;
+        const double* u = F[3 * f + d];
+        double a = 0.0;
+        for (int kk = 0; kk < pp; kk++)
+          for (int jj = 0; jj < pp; jj++) {
+            const double* row = u + (ea + (int64_t)N * ((eb + jj) + (int64_t)N * (ec + kk)));
+            const double yz = Y[jj] * Z[kk];
+            for (int ii = 0; ii < pp; ii++) a += row[ii] * X[ii] * yz;
+          }
+        dv[f] += a;
+      }
+    const double w = wg[gi] * wg[gj] * wg[gk];
+    s[0] += w * dv[0] * dv[0];
+    s[1] += w * dv[1] * dv[1];
+  }
+  __shared__ double red[2][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int k = 0; k < 2; k++) {
+    double v = s[k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[k][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double v = 0.0;
+    for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) v += red[threadIdx.x][w2];
+    atomicAdd(acc + threadIdx.x, v);
+  }
+}
+
 __global__ void fill_kernel(double* __restrict__ x, int64_t n, double v) {
   for (int64_t I = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; I < n; I += (int64_t)gridDim.x * blockDim.x) x[I] = v;
 }

@@ -485,3 +485,26 @@ def test_exp1_temporal_order_device_norms_64():
         errs.append(np.array(G.errors_uA(T)))
     ratio = errs[0][:2] / errs[1][:2]
     assert np.all((ratio > 3.3) & (ratio < 4.7)), (errs, ratio)
+
+
+@pytest.mark.parametrize("n,p", [(6, 1), (9, 2), (5, 3)])
+def test_divergence_closed_forms(n, p):
+    """NEXT-3 divergence diagnostic, pinned by B-spline reproduction (natural BC, no PEC
+    zeroing): Greville-abscissa coefficients reproduce linear functions exactly, so
+    E = (x, y, 0) has div E = 2 (L2 norm 2 on the unit cube) and H = (y, z, x) has div H = 0;
+    constant coefficients (partition of unity) give div = 0."""
+    N = n + p
+    t = np.concatenate([np.zeros(p + 1), np.arange(1, n) / n, np.ones(p + 1)])
+    xi = np.array([t[i + 1:i + p + 1].mean() for i in range(N)])
+    one = np.ones(N)
+    X = np.kron(np.kron(one, one), xi)  # flat i + N (j + N k): x fastest
+    Y = np.kron(np.kron(one, xi), one)
+    Z = np.kron(np.kron(xi, one), one)
+    G = adi.Patch(n, p, 0.1, bc=adi.ADI_BC_NATURAL)
+    G.set_fields([X, Y, np.zeros(N ** 3), Y, Z, X])
+    dE, dH = G.divergence()
+    assert abs(dE - 2.0) <= 1e-12 and dH <= 1e-12, (dE, dH)
+    c = np.ones(N ** 3)
+    G.set_fields([c, 2 * c, -c, 3 * c, c, c])
+    dE, dH = G.divergence()
+    assert dE <= 1e-12 and dH <= 1e-12, (dE, dH)
