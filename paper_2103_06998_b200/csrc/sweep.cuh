@@ -51,6 +51,11 @@ enum SweepMode { SW_MASS = 0, SW_MOD = 1, SW_DER = 2 };
 #ifndef ADI_SW_MOD_RECIP
 #define ADI_SW_MOD_RECIP 1
 #endif
+// Mass sweep: pass 1 stores the forward-eliminated y in `out` and pass 2 only
+// back-substitutes from it (1), instead of re-reading f and recomputing (0).
+#ifndef ADI_SW_MASS_Y
+#define ADI_SW_MASS_Y 0
+#endif
 #ifndef ADI_SW_MINB_MASS  // resident blocks the mass kernel's register budget is sized for
 #define ADI_SW_MINB_MASS 2
 #endif
@@ -137,6 +142,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
   constexpr int SWD = sw_state_words(MODE, P);
   constexpr int UW = MOD && P > 1 ? P - 1 : 1;  // stash width of U entries per row (pass 2)
   constexpr bool RECIP = MOD && SW_MOD_RECIP;     // pivots recomputed, not streamed
+  constexpr bool YST = MODE == SW_MASS && ADI_SW_MASS_Y;  // y stored by pass 1 (no recompute)
   static_assert(!DER || (RS >= 3 && CH >= P), "derivative mode needs the next chunk resident");
   extern __shared__ double sw_smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -511,6 +517,34 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       for (int r = 0; r < CH; r++) y[r] = xv[r];
     };
 
+    // store rows [r0, r0+CH) of the tile from y[] (x axis: transposed through slot sl)
+    auto store_chunk = [&](double* sl, int r0, const double* y) {
+      if (axis != 0) {
+        double* po = out + base + (int64_t)r0 * stride;
+#pragma unroll
+        for (int r = 0; r < CH; r++) {
+          if (fval && r0 + r < hi) *po = y[r];
+          po += stride;
+        }
+        if (YST) {
+#pragma unroll
+          for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
+        }
+      } else {
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
+        __syncwarp();
+        const int row = r0 + xr;
+        double* po = out + (int64_t)nx * f0 + row;
+#pragma unroll
+        for (int m = 0; m < CH; m++) {
+          const int ff = m * FPI + xf;
+          if (f0 + ff < NN && row < hi) po[(int64_t)nx * ff] = sl[xr * 33 + ff];
+        }
+      }
+    };
+
     // ---------------- pass 1: forward elimination, checkpoints ----------------
     // DER needs chunk c+1 resident while eliminating chunk c (window u_{k+P}).
     constexpr int AHEAD = DER ? 1 : 0;
@@ -526,6 +560,21 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       const double* nx = (DER && c + 1 < nc) ? ring + ((c + 1) % RS) * SLOT : nullptr;
       const int r0 = lo + c * CH;
       if (DER) der_prime(sl, r0);
+      if (YST) {
+        double y[CH];
+        if (chunk_fast(r0)) {
+          double yv[P + CH];
+          fwd_fast_cm(sl, nx, nullptr, yv);
+#pragma unroll
+          for (int r = 0; r < CH; r++) y[r] = yv[P + r];
+        } else {
+#pragma unroll
+          for (int r = 0; r < CH; r++) y[r] = 0.0;
+          fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, y, nullptr, nullptr);
+        }
+        __syncwarp();
+        store_chunk(const_cast<double*>(sl), r0, y);
+      } else {
       save_state(c);
       if (!MOD && chunk_fast(r0)) {
         double yv[P + CH];
@@ -534,6 +583,7 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
         fwd_chunk(std::true_type{}, sl, nx, nullptr, r0, nullptr, nullptr, nullptr);
       } else {
         fwd_chunk(std::false_type{}, sl, nx, nullptr, r0, nullptr, nullptr, nullptr);
+      }
       }
       __syncwarp();
       if (c + RS - 1 < nc) issue(c + RS - 1, 1);
@@ -566,7 +616,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
         }
       }
     };
-    load_prev(nc - 1);
+    if (YST) src[0] = out;  // pass 2 streams y back from out
+    else load_prev(nc - 1);
     if (DER) {
 #pragma unroll
       for (int c = 0; c < RS - 1; c++) {
@@ -581,13 +632,24 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
       __syncwarp();
       double* sl = ring + (c % RS) * SLOT;
       const int r0 = lo + c * CH;
-      set_state(nxt, pv, pc, r0);
-      if (c > 0) load_prev(c - 1);
+      if (!YST) {
+        set_state(nxt, pv, pc, r0);
+        if (c > 0) load_prev(c - 1);
+      }
       if (DER) der_prime(sl, r0);
       double y[CH];
       double us[CH * UW];  // u_{k,k+q}, q = 1..P-1 (u_{k,k+P} = a[2P] is recomputed)
       double ivs[RECIP ? CH : 1];  // recomputed pivots 1/u_kk of the chunk
-      if (!MOD && chunk_fast(r0)) {
+      if (YST && chunk_fast(r0)) {
+        double yv[P + CH];
+#pragma unroll
+        for (int r = 0; r < CH; r++) yv[P + r] = sl[r * 33 + lane];
+        bwd_fast_cm(yv, y);
+      } else if (YST) {
+#pragma unroll
+        for (int r = 0; r < CH; r++) y[r] = sl[r * 33 + lane];
+        bwd_chunk(std::false_type{}, sl, r0, y, us, ivs);
+      } else if (!MOD && chunk_fast(r0)) {
         double yv[P + CH];
         fwd_fast_cm(sl, nullptr, hd, yv);
         bwd_fast_cm(yv, y);
@@ -607,26 +669,8 @@ __global__ void __launch_bounds__(32 * SW_WARPS, MODE == SW_MASS ? ADI_SW_MINB_M
         for (int r = 0; r < CH; r++) y[r] = fma(coef, y[r], sl[(CH + r) * 33 + lane]);
       }
       // store the chunk
-      if (axis != 0) {
-        double* po = out + base + (int64_t)r0 * stride;
-#pragma unroll
-        for (int r = 0; r < CH; r++) {
-          if (fval && r0 + r < hi) *po = y[r];
-          po += stride;
-        }
-      } else {
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < CH; r++) sl[r * 33 + lane] = y[r];
-        __syncwarp();
-        const int row = r0 + xr;
-        double* po = out + (int64_t)nx * f0 + row;
-#pragma unroll
-        for (int m = 0; m < CH; m++) {
-          const int ff = m * FPI + xf;
-          if (f0 + ff < NN && row < hi) po[(int64_t)nx * ff] = sl[xr * 33 + ff];
-        }
-      }
+      if (YST) __syncwarp();
+      store_chunk(sl, r0, y);
       __syncwarp();
       // refill: MASS/MOD slot (c+1)%RS (chunk c+1 done) <- chunk c+1-RS; DER slot c%RS <- chunk c-(RS-1)
       if (DER) {
