@@ -186,15 +186,17 @@ def dist_init(force: bool = False):
     if ws > 1 or (force and "MASTER_ADDR" in os.environ):
         import torch.distributed as dist
 
-        backend = "nccl"
-        dist.init_process_group(backend=backend)
+        import torch
+
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        dist.init_process_group(backend="nccl", device_id=torch.device("cuda", local))
         return dist, dist.get_rank(), ws
     return None, 0, 1
 
 
 def run_reference(args, cfg):
-    dist, rank, ws = dist_init()
-    if rank != 0:
+    # rank 0 alone runs the CPU oracle; the other ranks exit without work (no collective)
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     sample_n = args.oracle_n
     rates = []
@@ -221,7 +223,7 @@ def run_reference(args, cfg):
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def config_dict(cfg, args):
@@ -423,11 +425,31 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clocks,
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
     S.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+_JSON_FD = None
+
+
+def emit(out):
+    """The one JSON line, to the process's original stdout (everything else -- NCCL's banner
+    included, which it writes to fd 1 -- goes to stderr; see main())."""
+    line = json.dumps(out) + "\n"
+    if _JSON_FD is None:
+        sys.stdout.write(line)
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line.encode())
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)  # C-level writes to stdout (NCCL, CUDA libraries) land on stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
