@@ -376,6 +376,7 @@ def run_ours(args, cfg):
     ms, e2e_ms = float(ms_t[0]), float(ms_t[1])
     if rank != 0:
         S.close()
+        dist.destroy_process_group()
         return
     dofs = dof_count(n, p)
     value = dofs * args.steps / (ms * 1e-3)  # the whole patch (all ranks together)
@@ -406,7 +407,7 @@ def run_ours(args, cfg):
     # end-to-end HBM fraction of the step (algorithmic bytes of the schedule run)
     sbytes = step_bytes(n, p)
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and ws == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
         rate, dt, desc = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
     out = {
