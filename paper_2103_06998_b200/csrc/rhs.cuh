@@ -62,7 +62,10 @@ constexpr int RX_TY = 16;
 constexpr int RX_THREADS = 256;  // 32 x 8, two output rows each
 constexpr int RX_MAXT = 4;
 constexpr int RX_RING = 3;
-constexpr int RX_KCMAX = 64;  // max z-chunk (rows of the per-block z-coefficient table)
+#ifndef ADI_RX_KCMAX
+#define ADI_RX_KCMAX 64
+#endif
+constexpr int RX_KCMAX = ADI_RX_KCMAX;  // max z-chunk (rows of the per-block z-coefficient table)
 
 struct RhsArgs {
   int N;                      // global extent (x, y: the arrays' extents; z: of the patch)
