@@ -452,7 +452,7 @@ def test_exp1_paper_bounds_on_gpu(tau_key, l2_key, hc_key, tau):
     assert mx[2] < gv[hc_key] and mx[3] < gv[hc_key], mx
 
 
-@pytest.mark.parametrize("n,p", [(5, 1), (9, 2), (6, 3), (4, 5)])
+@pytest.mark.parametrize("n,p", [(1, 1), (2, 3), (5, 1), (9, 2), (6, 3), (4, 5)])
 def test_errors_uA_device_vs_oracle(n, p):
     """NEXT-3: adi_errors_uA (device quadrature, q = p+3) equals the oracle's norms of the
     same coefficients, at t = 0 (projection error only) and after steps."""

@@ -115,9 +115,10 @@ def _gpu_case(n, p, seed, inplace=False):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n,p", [(7, 1), (37, 2), (40, 3), (21, 4), (13, 5)])
+@pytest.mark.parametrize("n,p", [(1, 1), (1, 5), (2, 2), (7, 1), (37, 2), (40, 3), (21, 4), (13, 5)])
 def test_project_weighted_parity(n, p):
-    """Several 32-fiber tiles and sweep chunks, ragged tails (N odd/even), every degree."""
+    """Degenerate single-element patches, several 32-fiber tiles and sweep chunks, ragged tails
+    (N odd/even), every degree."""
     assert _gpu_case(n, p, 10 + p) <= TOL
 
 
