@@ -49,34 +49,35 @@ def dof_count(n: int, p: int) -> int:
     return 3 * N * (N - 2) ** 2 + 3 * N ** 3
 
 
-def algorithmic_bytes(n: int, p: int):
-    """Algorithmic HBM bytes per launch of each kernel class.
-
-    Units: U = N^3 coefficients; Ue = N (N-2)^2 active rows of an E component.
-      rhs_e      : one component per launch: read E_d, H_{d+1}, H_{d+2}, E_sigma, a, c; write R_d -> 7 U * 8 B
-      rhs_h      : (general mu only) read H_d, Eo, En, b; write G_d -> 5 U * 8 B
-      sweep_mass : 16 B per active row (read rhs, write solution); 3 jobs per launch
-      sweep_mod  : 24 B per active row (read rhs and c, write solution); 3 jobs per launch
-      sweep_der  : 24 B per row (read u and base, write out); 3 jobs of U rows per launch
-    Per step with uniform mu: 4 mass launches on E sets, 2 row-modified, 4 derivative-projection.
-    """
+def step_class_bytes(n: int, p: int, mu_uniform: bool = True):
+    """Algorithmic HBM bytes of one time step per kernel class, in SURVEY.md §8(a)/§8(d)'s
+    counting (compulsory traffic of each hot-path step, independent of how many launches the
+    schedule spends on it).  U = N^3 stored coefficients; Ue = N (N-2)^2 active rows of an E
+    component (PEC, D1).  Per substep:
+      rhs_e      (a1/a5): read E1..E3, H1..H3, a, c; write R1..R3            -> 11 U words
+      sweep_mod  (a2/a6 first sweep): 24 B per active row (read f, c; write x), 3 components -> 9 Ue
+      sweep_mass (a2/a6 other two sweeps): 16 B per active row, 2 x 3 components       -> 12 Ue
+      sweep_der  (a3+a4 / a7+a8, uniform mu: the exact derivative-projection identity of
+                  SURVEY §8(a)'s note): 24 B per row (read u, base; write out), 2 x 3 -> 18 U
+      rhs_h      (general mu only, a3/a7): read H_d, Eo, En, b; write G_d, 3 components -> 15 U
+                  (then 9 mass sweeps over H: 18 U, counted under sweep_mass)
+    Uniform mu: 29 U + 21 Ue words per substep, i.e. (58 U + 42 Ue) * 8 B per step."""
     N = n + p
     U = N ** 3
     Ue = N * (N - 2) ** 2
-    return {
-        "rhs_e": 7 * U * 8.0,
-        "rhs_h": 5 * U * 8.0,
-        "sweep_mass": 16.0 * 3 * Ue,
-        "sweep_mod": 24.0 * 3 * Ue,
-        "sweep_der": 24.0 * 3 * U,
-    }
+    w = 8.0
+    out = {"rhs_e": 2 * 11 * U * w, "sweep_mod": 2 * 9 * Ue * w, "sweep_mass": 2 * 12 * Ue * w}
+    if mu_uniform:
+        out["sweep_der"] = 2 * 18 * U * w
+    else:
+        out["rhs_h"] = 2 * 15 * U * w
+        out["sweep_mass"] += 2 * 18 * U * w
+    return out
 
 
 def step_bytes(n: int, p: int) -> float:
-    """Algorithmic HBM bytes of one step of the schedule run (uniform mu):
-    per substep 3 rhs_e (7U) + 1 mod + 2 mass launches (3 jobs each) + 2 derivative launches."""
-    a = algorithmic_bytes(n, p)
-    return 2 * (3 * a["rhs_e"] + a["sweep_mod"] + 2 * a["sweep_mass"] + 2 * a["sweep_der"])
+    """Compulsory HBM bytes of one step of the schedule run (uniform mu): (58 U + 42 Ue) * 8 B."""
+    return sum(step_class_bytes(n, p).values())
 
 
 def hbm_peak():
@@ -160,23 +161,78 @@ def make_inputs(cfg, seed=12345, pinned=False):
     return eps, fields
 
 
-def cpu_oracle_rate(cfg, steps: int, sample_n: int):
-    """The oracle as it stands (oracle/, one core) on a bounded sample of the workload:
-    the same recipe at n = sample_n.  Returns (DOF-updates/s, seconds, description)."""
+def host_info():
+    """Host CPU facts reported next to the one-core oracle number."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"host_cores": os.cpu_count(), "cpu_model": model}
+
+
+def pin_one_core():
+    """Pin this process to one core (the oracle is single-threaded by definition); returns the
+    previous affinity mask so it can be restored."""
+    try:
+        old = os.sched_getaffinity(0)
+        core = min(old)
+        os.sched_setaffinity(0, {core})
+        return old, core
+    except (AttributeError, OSError):
+        return None, None
+
+
+def cpu_oracle_rate(cfg, steps: int, sample_n: int, repeats: int = 5):
+    """The oracle as it stands (oracle/, one core, pinned) on a bounded sample of the workload:
+    the same recipe at n = sample_n, `repeats` timed regions of `steps` steps each (median).
+    Returns (DOF-updates/s, seconds per region, description, extra facts)."""
     import oracle
 
     n, p = sample_n, cfg["p"]
     N = n + p
-    P = oracle.Patch(n, p, cfg["tau"])
-    P.set_materials(workloads.element_eps(n, cfg["material"]))
-    P.set_fields(workloads.random_fields(N, 1))
-    t0 = time.perf_counter()
-    P.step(steps)
-    dt = time.perf_counter() - t0
+    old, core = pin_one_core()
+    try:
+        P = oracle.Patch(n, p, cfg["tau"])
+        P.set_materials(workloads.element_eps(n, cfg["material"]))
+        P.set_fields(workloads.random_fields(N, 1))
+        times = []
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            P.step(steps)
+            times.append(time.perf_counter() - t0)
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    dt = float(np.median(times))
     rate = dof_count(n, p) * steps / dt
-    desc = (f"{cfg['name']} recipe at n={n} (N={N}, {dof_count(n, p)} DOF), {steps} step(s), "
-            f"single-threaded C oracle, setup excluded")
-    return rate, dt, desc
+    desc = (f"{cfg['name']} recipe at n={n} (N={N}, {dof_count(n, p)} DOF), median of {repeats} timed regions "
+            f"of {steps} step(s), single-threaded C oracle pinned to core {core}, setup excluded")
+    extra = dict(host_info(), pinned_core=core, seconds_per_region=times)
+    return rate, dt, desc, extra
+
+
+def parity_probe(cfg, n_small: int = 16, steps: int = 2):
+    """A small in-run parity number: the bench recipe at n = n_small, `steps` steps, library vs
+    oracle on identical seeded inputs (relative L2 per field, D16)."""
+    import oracle
+    import paper_2103_06998_b200 as adi
+
+    n, p, tau = n_small, cfg["p"], cfg["tau"]
+    N = n + p
+    eps = workloads.element_eps(n, cfg["material"])
+    f = workloads.random_fields(N, 77)
+    outs = []
+    for P in (adi.Patch(n, p, tau), oracle.Patch(n, p, tau)):
+        P.set_materials(eps)
+        P.set_fields(f)
+        P.step(steps)
+        outs.append(P.get_fields())
+    errs = [float(np.linalg.norm(a - b) / np.linalg.norm(b)) for a, b in zip(*outs)]
+    return {"max_rel_l2": max(errs), "case": f"{cfg['name']} recipe at n={n}, {steps} steps, GPU vs oracle"}
 
 
 def dist_init(force: bool = False):
@@ -205,6 +261,7 @@ def run_reference(args, cfg):
 
     n, p = sample_n, cfg["p"]
     N = n + p
+    old_aff, core = pin_one_core()
     P = oracle.Patch(n, p, cfg["tau"])
     P.set_materials(workloads.element_eps(n, cfg["material"]))
     P.set_fields(workloads.random_fields(N, 1))
@@ -212,18 +269,29 @@ def run_reference(args, cfg):
     t0 = time.perf_counter()
     P.step(args.steps)
     dt = time.perf_counter() - t0
+    if old_aff is not None:
+        os.sched_setaffinity(0, old_aff)
     rate = dof_count(n, p) * args.steps / dt
     desc = (f"{cfg['name']} recipe at n={n} (N={N}), {args.steps} timed steps after {args.warmup} warm-up, "
-            f"single-threaded C oracle")
+            f"single-threaded C oracle pinned to core {core}")
     out = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": config_dict(cfg, args),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "cpu_baseline": dict({"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+                             **host_info()),
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(out)
+
+
+def parallelism_label(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws == 1 and not args.slabs:
+        return "single GPU, whole patch, CUDA graph per step"
+    return (f"z-slab decomposition over {ws} rank(s) (one process per GPU): NCCL halo exchange before the "
+            "RHS, all-to-all z<->y transposes around z-sweeps (paper_2103_06998_b200.dist)")
 
 
 def config_dict(cfg, args):
@@ -233,9 +301,7 @@ def config_dict(cfg, args):
                      f"material={cfg['material']}, seeded random fields"),
         "n": n, "p": p, "N": n + p, "tau": cfg["tau"], "dof_per_step": dof_count(n, p),
         "l2_policy": "inputs larger than L2 (each field %.2f GB > 126 MB)" % ((n + p) ** 3 * 8 / 1e9),
-        "parallelism": ("single GPU, whole patch, CUDA graph per step" if args.gpus == 1 else
-                        f"z-slab decomposition over {args.gpus} GPUs: NCCL halo exchange before the RHS, "
-                        "all-to-all z<->y transposes around z-sweeps (paper_2103_06998_b200.dist)"),
+        "parallelism": parallelism_label(args),
     }
 
 
@@ -353,7 +419,8 @@ def run_ours(args, cfg):
     clocks = clk.summary()
     # ---------------- per-kernel breakdown (same steps, each launch bracketed by events) ----
     S.timing(True)
-    S.step(max(1, min(args.steps, 3)))
+    S.timed_steps = max(1, min(args.steps, 3))
+    S.step(S.timed_steps)
     rep = S.report()
     S.timing(False)
     lps = S.launches_per_step()
@@ -381,18 +448,22 @@ def run_ours(args, cfg):
     dofs = dof_count(n, p)
     value = dofs * args.steps / (ms * 1e-3)  # the whole patch (all ranks together)
     e2e_value = dofs * args.steps / (e2e_ms * 1e-3)
-    # roofline of the dominant kernel class
+    # roofline of the dominant kernel class: survey bytes of the class per step, divided over
+    # the class's launches per step (rep covers `timed_steps` steps)
     peak, peak_src = hbm_peak()
-    algo = algorithmic_bytes(n, p)
+    cls_bytes = step_class_bytes(n, p)
+    algo = {k: v * S.timed_steps / rep[k][1] for k, v in cls_bytes.items() if rep.get(k, (0, 0))[1] > 0}
     cls = max(algo, key=lambda k: rep[k][0])
     t_cls, n_cls = rep[cls]
     achieved = algo[cls] / (t_cls * 1e-3 / n_cls) / 1e9
     traffic = None
+    traffic_src = None
     try:
         with open(TRAFFIC_PATH) as f:
             tr = json.load(f)
         if tr.get("config") == cfg["name"] and cls in tr.get("bytes_per_launch", {}):
             traffic = tr["bytes_per_launch"][cls]
+            traffic_src = tr.get("source")
     except Exception:
         pass
     kernels = {}
@@ -401,6 +472,7 @@ def run_ours(args, cfg):
             continue
         kd = {"ms_total": t, "launches": cnt, "share": t / sum(v[0] for v in rep.values())}
         if k in algo:
+            kd["algorithmic_bytes_per_launch"] = algo[k]
             kd["achieved_gbs"] = algo[k] / (t * 1e-3 / cnt) / 1e9
             kd["frac"] = kd["achieved_gbs"] / peak
         kernels[k] = kd
@@ -408,15 +480,18 @@ def run_ours(args, cfg):
     sbytes = step_bytes(n, p)
     cpu = None
     if not args.no_cpu_baseline and ws == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
-        rate, dt, desc = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)
-        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt}
+        rate, dt, desc, extra = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)
+        cpu = dict({"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc, "seconds": dt},
+                   **extra)
+    parity = parity_probe(cfg) if ws == 1 else None
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, args),
         "roofline": {"bound": "hbm", "kernel": cls, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": algo[cls]},
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": algo[cls],
+                     "bytes_basis": "SURVEY §8(a)/(d) compulsory bytes of the class per step / launches per step"},
         "step_hbm_frac": (sbytes / (ms * 1e-3 / args.steps) / 1e9) / peak,
         "step_algorithmic_bytes": sbytes,
         "kernels": kernels,
@@ -425,6 +500,7 @@ def run_ours(args, cfg):
                 "ms": e2e_ms, "note": "set_fields(pinned host) + step(K) via CUDA graph + get_fields(pinned host)"},
         "gpu_launches": launches,
         "clocks": clocks,
+        "parity": parity,
     }
     emit(out)
     S.close()
@@ -459,7 +535,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--oracle-n", type=int, default=64,
                     help="n of the bounded CPU-oracle sample (c5 recipe at n=64: ~2 s per oracle step)")
-    ap.add_argument("--oracle-steps", type=int, default=8)
+    ap.add_argument("--oracle-steps", type=int, default=2,
+                    help="steps per timed oracle region (5 regions, median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true",
                     help="use the slab-decomposed path (paper_2103_06998_b200.dist) even on one GPU")

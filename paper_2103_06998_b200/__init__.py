@@ -157,14 +157,28 @@ class AdiError(RuntimeError):
         self.status = status
 
 
-def _addr(x) -> int:
-    """Address of a host numpy array or a torch tensor (host or CUDA)."""
+def _addr(x, count: int | None = None, what: str = "array") -> int:
+    """Address of a host numpy array or a torch tensor (host or CUDA) of float64 entries.
+
+    Raises ValueError (not assert: the checks must survive ``python -O``) unless the array is
+    C-contiguous float64 and, when ``count`` is given, holds exactly ``count`` entries -- the
+    library copies ``count`` doubles from / to the pointer."""
     if isinstance(x, np.ndarray):
-        assert x.dtype == np.float64 and x.flags["C_CONTIGUOUS"], "need contiguous float64"
-        return x.ctypes.data
-    # torch.Tensor
-    assert x.dtype.itemsize == 8 and x.is_contiguous(), "need contiguous float64 tensor"
-    return x.data_ptr()
+        if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{what}: need a C-contiguous float64 array, got {x.dtype}")
+        n = x.size
+        addr = x.ctypes.data
+    else:  # torch.Tensor
+        import torch
+        if not isinstance(x, torch.Tensor):
+            raise ValueError(f"{what}: need a numpy array or a torch tensor, got {type(x).__name__}")
+        if x.dtype != torch.float64 or not x.is_contiguous():
+            raise ValueError(f"{what}: need a contiguous float64 tensor, got {x.dtype}")
+        n = x.numel()
+        addr = x.data_ptr()
+    if count is not None and n != count:
+        raise ValueError(f"{what}: {n} entries, expected {count}")
+    return addr
 
 
 def _as_f64(x):
@@ -173,10 +187,10 @@ def _as_f64(x):
     return x
 
 
-def _ptr_array(objs):
+def _ptr_array(objs, count: int | None = None, what: str = "array"):
     arr = (C.c_void_p * len(objs))()
     for i, o in enumerate(objs):
-        arr[i] = None if o is None else _addr(o)
+        arr[i] = None if o is None else _addr(o, count, f"{what}[{i}]")
     return arr
 
 
@@ -215,29 +229,44 @@ class Patch:
         self._check(self._L.adi_set_tau(self.h, float(tau)))
         self.tau = float(tau)
 
+    @property
+    def local_count(self) -> int:
+        """Entries of one field held by this patch (the local slab N x N x (k1 - k0))."""
+        N, k0, k1 = self.layout()
+        return N * N * (k1 - k0)
+
     def set_materials(self, eps_elem, mu_elem=None):
+        ne = self.n ** 3
         e, m = _as_f64(eps_elem), (None if mu_elem is None else _as_f64(mu_elem))
-        self._check(self._L.adi_set_materials(self.h, _addr(e), None if m is None else _addr(m)))
+        self._check(self._L.adi_set_materials(self.h, _addr(e, ne, "eps_elem"),
+                                              None if m is None else _addr(m, ne, "mu_elem")))
 
     def set_materials_tf(self, eps_tf, mu_tf=None):
         e, m = _as_f64(eps_tf), (None if mu_tf is None else _as_f64(mu_tf))
-        self._check(self._L.adi_set_materials_tf(self.h, _addr(e), None if m is None else _addr(m)))
+        self._check(self._L.adi_set_materials_tf(self.h, _addr(e, self.U, "eps_tf"),
+                                                 None if m is None else _addr(m, self.U, "mu_tf")))
 
     def set_fields(self, fields):
         fs = [_as_f64(f) for f in fields]
-        assert len(fs) == 6
-        self._check(self._L.adi_set_fields(self.h, _ptr_array(fs)))
+        if len(fs) != 6:
+            raise ValueError(f"set_fields: need 6 fields, got {len(fs)}")
+        self._check(self._L.adi_set_fields(self.h, _ptr_array(fs, self.local_count, "fields")))
 
     def get_fields(self, out=None):
         if out is None:
-            out = [np.empty(self.U) for _ in range(6)]
-        self._check(self._L.adi_get_fields(self.h, _ptr_array(out)))
+            out = [np.empty(self.local_count) for _ in range(6)]
+        if len(out) != 6:
+            raise ValueError(f"get_fields: need 6 output arrays, got {len(out)}")
+        self._check(self._L.adi_get_fields(self.h, _ptr_array(out, self.local_count, "out")))
         return out
 
     def set_source(self, loads, signal):
+        if len(loads) != 3:
+            raise ValueError("set_source: need 3 load vectors (or None)")
         ls = [None if l is None else _as_f64(l) for l in loads]
         sig = _as_f64(signal)
-        self._check(self._L.adi_set_source(self.h, _ptr_array(ls), _addr(sig), int(len(sig))))
+        self._check(self._L.adi_set_source(self.h, _ptr_array(ls, self.U, "loads"), _addr(sig, None, "signal"),
+                                           int(len(sig))))
 
     def set_point_source(self, comp: int, pos, signal):
         sig = _as_f64(signal)
@@ -374,13 +403,14 @@ class Patch:
     def sweep(self, comp: int, axis: int, modified: bool, rhs):
         r = _as_f64(rhs)
         out = np.zeros(self.U)
-        self._check(self._L.adi_debug_sweep(self.h, int(comp), int(axis), int(bool(modified)), _addr(r), _addr(out)))
+        self._check(self._L.adi_debug_sweep(self.h, int(comp), int(axis), int(bool(modified)), _addr(r, self.U, "rhs"),
+                                            _addr(out)))
         return out
 
     def solve_e(self, s: int, d: int, rhs):
         r = _as_f64(rhs)
         out = np.zeros(self.U)
-        self._check(self._L.adi_debug_solve_e(self.h, int(s), int(d), _addr(r), _addr(out)))
+        self._check(self._L.adi_debug_solve_e(self.h, int(s), int(d), _addr(r, self.U, "rhs"), _addr(out)))
         return out
 
     def rhs_e(self, s: int):

@@ -1141,9 +1141,10 @@ adi_status adi_set_tau(adi_patch P, double tau) {
   P->tau = tau;
   adi_status st = derive_abc(P, P->epsh, P->muh);
   if (!st) st = factorize(P);
-  if (st) {
+  if (st) {  // strong guarantee: a, b, c AND the six pivot caches back to the previous tau
     P->tau = old;
     derive_abc(P, P->epsh, P->muh);
+    factorize(P);
     cudaStreamSynchronize(P->stream);
     return poison(P, st);
   }
@@ -1156,10 +1157,11 @@ static adi_status set_tf(adi_patch P, double* eps_new, double* mu_new) {
   std::swap(P->muh, mu_new);
   adi_status st = derive_abc(P, P->epsh, P->muh);
   if (!st) st = factorize(P);
-  if (st) {  // restore
+  if (st) {  // restore a, b, c and re-derive the pivot caches of the previous materials
     std::swap(P->epsh, eps_new);
     std::swap(P->muh, mu_new);
     derive_abc(P, P->epsh, P->muh);
+    factorize(P);
   }
   cudaStreamSynchronize(P->stream);
   cudaFree(eps_new);

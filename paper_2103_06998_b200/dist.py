@@ -180,6 +180,10 @@ class DistPatch:
         self.loads = [None, None, None]
         self.signal = None
         self.step_index = 0
+        if self.stream is not None:
+            # the buffers above were allocated and zero-filled on the current stream; every later
+            # use is on self.stream, so order it after those fills
+            self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.set_materials_tf(torch.ones(N ** 3, dtype=torch.float64, device=self.device), None)
 
     def _on_stream(self):

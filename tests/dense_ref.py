@@ -130,3 +130,100 @@ class DenseMaxwell:
         ]
         H1 = [np.linalg.solve(Mass, g) for g in G]
         return E1, H1
+
+    # ------------------------------------------------------------------------
+    # Control scheme for pin P5: the first-order
+    # Peaceman-Rachford ADI in (E, H) with the SAME Galerkin blocks, solved as
+    # coupled block systems (no substitution, hence the exact Schur complement
+    # -C1 M^-1 C2' where the paper's discrete1/discrete3 put the stiffness K).
+    # Substep 1 is implicit in C1 H and C2 E, substep 2 in C2 H and C1 E
+    # (scheme1a-scheme1d):
+    #   M E^h - a C1 H^h = M E^n - a C2 H^n ,   M H^h - b C2' E^h = M H^n - b C1' E^n
+    #   M E^1 + a C2 H^1 = M E^h + a C1 H^h ,   M H^1 + b C1' E^1 = M H^h + b C2' E^h
+    # with (C1 H)_1 = d2 H3, (C1 H)_2 = d3 H1, (C1 H)_3 = d1 H2 and
+    #      (C2 H)_1 = d3 H2, (C2 H)_2 = d1 H3, (C2 H)_3 = d2 H1; the primed
+    # operators are the same derivatives with H test functions and E trial functions.
+    # ------------------------------------------------------------------------
+    def curl_blocks(self):
+        """Dense Galerkin blocks of C1, C2 (E test / H trial) and C1', C2' (H test / E trial) as
+        dicts {(row component, column component): matrix}, components 0..2 of E resp. H."""
+        Adv = [self.form(self.Phi, self.D[ax]) for ax in range(3)]  # (d_ax trial, V)
+        C1 = {(0, 2): Adv[1], (1, 0): Adv[2], (2, 1): Adv[0]}
+        C2 = {(0, 1): Adv[2], (1, 2): Adv[0], (2, 0): Adv[1]}
+        return C1, C2, dict(C1), dict(C2)
+
+    def pr_operators(self, a, b):
+        """Block matrices over the unknowns (E1, E2, E3 on their active sets, H1, H2, H3):
+        Mb = blockdiag(M), and for substep s the implicit / explicit operators
+        L1 = Mb - T1, R1 = Mb + T2 (substep 1) and L2 = Mb - T2, R2 = Mb + T1 (substep 2),
+        T1 = [[0, a C1], [b C2', 0]], T2 = [[0, -a C2], [-b C1', 0]] (row-scaled by the
+        test function's a = tau/(2 eps), b = tau/(2 mu), D5)."""
+        U = self.U
+        masks = [self.active(d) for d in range(3)] + [np.ones(U, bool)] * 3
+        off = np.cumsum([0] + [int(m.sum()) for m in masks])
+        n = off[-1]
+        Mass = self.form(self.Phi, self.Phi)
+        C1, C2, C1p, C2p = self.curl_blocks()
+        Mb, T1, T2 = np.zeros((n, n)), np.zeros((n, n)), np.zeros((n, n))
+        for c in range(6):
+            m = masks[c]
+            Mb[off[c]:off[c + 1], off[c]:off[c + 1]] = Mass[np.ix_(m, m)]
+
+        def put(T, r, c, X, scale):
+            mr, mc = masks[r], masks[c]
+            T[off[r]:off[r + 1], off[c]:off[c + 1]] += scale[mr][:, None] * X[np.ix_(mr, mc)]
+
+        for (i, j), X in C1.items():
+            put(T1, i, 3 + j, X, a)
+        for (i, j), X in C2p.items():
+            put(T1, 3 + i, j, X, b)
+        for (i, j), X in C2.items():
+            put(T2, i, 3 + j, X, -a)
+        for (i, j), X in C1p.items():
+            put(T2, 3 + i, j, X, -b)
+        return masks, off, Mb, T1, T2
+
+    def pr_energy(self, E, H, a, b):
+        """Et(u) = u^T Mb u + ||T2 u||^2_{Mb^-1} = ||(Mb - T2) u||^2_{Mb^-1} (T2 skew for
+        eps = mu = 1), evaluated block by block without forming the block matrices."""
+        Mass = self.form(self.Phi, self.Phi)
+        C1, C2, C1p, _ = self.curl_blocks()
+        a = np.broadcast_to(a, self.U)
+        b = np.broadcast_to(b, self.U)
+        masks = [self.active(d) for d in range(3)] + [np.ones(self.U, bool)] * 3
+        f = [np.where(m, np.asarray(x, dtype=float), 0.0) for x, m in zip(list(E) + list(H), masks)]
+        em = sum(float(x @ Mass @ x) for x in f)
+        t2 = [np.zeros(self.U) for _ in range(6)]
+        for (i, j), X in C2.items():  # E rows: -a C2 H
+            t2[i] -= a * (X @ f[3 + j])
+        for (i, j), X in C1p.items():  # H rows: -b C1' E
+            t2[3 + i] -= b * (X @ f[j])
+        extra = 0.0
+        for c in range(6):
+            m = masks[c]
+            extra += float(t2[c][m] @ np.linalg.solve(Mass[np.ix_(m, m)], t2[c][m]))
+        return em, em + extra
+
+    def step_pr(self, E, H, a, b, steps=1):
+        """`steps` steps of the exact-Schur Peaceman-Rachford control; returns (E, H, Et) where
+        Et[k] = ||(Mb - T2) u^k||^2_{Mb^-1}, the quadratic form the scheme conserves for
+        eps = mu = 1 (each half step is a Cayley transform of a skew operator)."""
+        masks, off, Mb, T1, T2 = self.pr_operators(np.broadcast_to(a, self.U), np.broadcast_to(b, self.U))
+        u = np.concatenate([np.asarray(f, dtype=float)[m] for f, m in zip(list(E) + list(H), masks)])
+        L1, R1, L2, R2 = Mb - T1, Mb + T2, Mb - T2, Mb + T1
+
+        def energy(v):
+            w = L2 @ v
+            return float(w @ np.linalg.solve(Mb, w))
+
+        Et = [energy(u)]
+        for _ in range(steps):
+            u = np.linalg.solve(L1, R1 @ u)
+            u = np.linalg.solve(L2, R2 @ u)
+            Et.append(energy(u))
+        out = []
+        for c in range(6):
+            f = np.zeros(self.U)
+            f[masks[c]] = u[off[c]:off[c + 1]]
+            out.append(f)
+        return out[:3], out[3:], Et

@@ -1,0 +1,59 @@
+"""Full-horizon parity on the north-star configs against stored oracle results (row 18).
+
+The goldens tests/golden/<cfg>_golden.npz are written by tools/make_golden.py, which calls only
+``oracle/`` and ``workloads/`` (no value comes from the CUDA path): c3 after all 200 steps, c4
+after all 500 steps, c5 (512^3, the bench configuration) after 1 step.  Here the library
+regenerates the same seeded inputs, steps the same number of times on the GPU and is compared
+on the stored data (D16, tolerance 1e-10 from BASELINE.json's north_star):
+  * sampled relative L2 per field: ||g_S - o_S|| / ||o_S|| <= 1e-10 over the stored sample S
+    (half seeded-uniform indices, half the indices of the largest |o|);
+  * the norm of the whole coefficient vector: | ||g|| - ||o|| | <= 1e-10 ||o||;
+  * element-wise on the sample: |g_i - o_i| <= 1e-10 max|o|.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2103_06998_b200 as adi
+from tools.make_golden import inputs
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 1e-10
+
+
+def _run_gpu(name):
+    I = inputs(name)
+    G = adi.Patch(I["n"], I["p"], I["tau"])
+    G.set_materials(I["eps"])
+    G.set_fields(I["fields"])
+    del I["fields"]
+    if I["source"] is not None:
+        comp, pos, sig = I["source"]
+        G.set_point_source(comp, pos, sig)
+    G.step(I["steps"])
+    out = G.get_fields()
+    G.close()
+    return I, out
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_golden_full_horizon(name):
+    path = os.path.join(GOLD, f"{name}_golden.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tools/make_golden.py {name}")
+    gd = np.load(path)
+    I, out = _run_gpu(name)
+    assert int(gd["steps"]) == I["steps"] and int(gd["n"]) == I["n"] and int(gd["p"]) == I["p"]
+    report = []
+    for c in range(6):
+        idx, ref = gd[f"idx{c}"], gd[f"val{c}"]
+        got = out[c][idx]
+        rel_s = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        rel_n = abs(np.linalg.norm(out[c]) - gd["norm"][c]) / gd["norm"][c]
+        elem = np.abs(got - ref).max() / gd["maxabs"][c]
+        report.append((c, rel_s, rel_n, elem))
+    print(name, "field, sampled rel L2, rel norm diff, max elem / max|o|:", report)
+    for c, rel_s, rel_n, elem in report:
+        assert rel_s <= TOL and rel_n <= TOL and elem <= TOL, (name, c, rel_s, rel_n, elem)

@@ -508,3 +508,24 @@ def test_divergence_closed_forms(n, p):
     G.set_fields([c, 2 * c, -c, 3 * c, c, c])
     dE, dH = G.divergence()
     assert dE <= 1e-12 and dH <= 1e-12, (dE, dH)
+
+
+def test_set_tau_singular_keeps_state():
+    """ADI_ERR_SINGULAR from the D12 pivot gate leaves the previous state intact (strong
+    guarantee of §8(b)): natural BC keeps the full index range, where S is singular (S 1 = 0), so
+    a huge tau (c = tau^2/4 ~ 1e19) makes M + c S numerically singular; afterwards the patch
+    still steps exactly like the oracle at the old tau (a, b, c and the pivot caches restored)."""
+    n, p, tau = 5, 2, 0.05
+    G = adi.Patch(n, p, tau, bc=adi.ADI_BC_NATURAL)
+    O = oracle.Patch(n, p, tau, 1)
+    f = workloads.random_fields(n + p, 61)
+    eps = workloads.element_eps(n, "random", seed=4)
+    for X in (G, O):
+        X.set_materials(eps)
+        X.set_fields(f)
+    with pytest.raises(adi.AdiError) as e:
+        G.set_tau(1e10)
+    assert e.value.status == adi.ADI_ERR_SINGULAR
+    G.step(2)
+    O.step(2)
+    assert max(rel(a, b) for a, b in zip(G.get_fields(), O.get_fields())) <= TOL_STEP

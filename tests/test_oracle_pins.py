@@ -201,12 +201,12 @@ def test_P1d_bruteforce_3d(p):
 # ---------------------------------------------------------------------------
 # P2: one and three full steps against the dense brute force from weak1-weak4
 # ---------------------------------------------------------------------------
-def _dense_vs_oracle(n, p, tau, material, steps, seed, source=False):
+def _dense_vs_oracle(n, p, tau, material, steps, seed, source=False, bc=0):
     N = n + p
     U = N ** 3
     rng = np.random.default_rng(seed)
     fields = workloads.random_fields(N, seed)
-    P = oracle.Patch(n, p, tau)
+    P = oracle.Patch(n, p, tau, bc)
     if material == "uniform":
         eps_tf, mu_tf = np.ones(U), np.ones(U)
     else:
@@ -221,7 +221,7 @@ def _dense_vs_oracle(n, p, tau, material, steps, seed, source=False):
         sig = rng.uniform(-1, 1, steps)
         P.set_source(J, sig)
     P.set_fields(fields)
-    D = DenseMaxwell(n, p, tau)
+    D = DenseMaxwell(n, p, tau, pec=(bc == 0))
     E = [f.copy() for f in fields[:3]]
     H = [f.copy() for f in fields[3:]]
     for k in range(steps):
@@ -246,6 +246,36 @@ def test_P2_dense_three_steps_source(p):
 
 def test_P2_dense_5cubed():
     assert _dense_vs_oracle(5, 1, 0.02, "random", 1, seed=33) <= 1e-10
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_P2_dense_natural_bc(p):
+    """NATURAL BC (SPEC default, NEXT-2): no coefficient eliminated; the oracle's bc=1 step
+    equals the dense weak-form brute force on the full index sets (1 and 2 steps, random
+    per-test-function eps and mu, with a source)."""
+    n = 3
+    assert _dense_vs_oracle(n, p, 0.05, "random", 1, seed=40 + p, bc=1) <= 1e-10
+    assert _dense_vs_oracle(n, p, 0.1, "random", 2, seed=50 + p, source=True, bc=1) <= 1e-10
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_point_load_vs_scipy(p):
+    """orc_point_load (the oracle side of every c3/c4 source, D9): J_rst = B_r(x) B_s(y) B_t(z),
+    against scipy's independent B-spline evaluation, incl. points on knots and on the boundary."""
+    n = 5
+    P = oracle.Patch(n, p, 0.01)
+    N = P.N
+    t = np.concatenate([np.zeros(p + 1), np.arange(1, n) / n, np.ones(p + 1)])
+    spl = BSpline(t, np.eye(N), p, extrapolate=False)
+    rng = np.random.default_rng(p)
+    pts = [tuple(rng.uniform(0, 1, 3)) for _ in range(5)] + [(0.2, 0.4, 0.6), (0.0, 0.5, 1.0 - 1e-16),
+                                                             workloads.dipole_position(n)]
+    for x, y, z in pts:
+        got = P.point_load(x, y, z)
+        bx, by, bz = (np.nan_to_num(spl(v)) for v in (x, y, z))
+        ref = np.kron(np.kron(bz, by), bx)  # index i + N (j + N k)
+        assert np.allclose(got, ref, rtol=0, atol=1e-14), (x, y, z)
+        assert abs(got.sum() - 1.0) <= 1e-13  # partition of unity in every axis
 
 
 # ---------------------------------------------------------------------------
@@ -401,8 +431,9 @@ def _run_uA(n, p, tau, steps):
 
 @pytest.mark.slow
 def test_P4_temporal_order_c2_taus():
-    """c2's tau set {1e-2, 5e-3, 2.5e-3}, compared at the common time t = 0.25."""
-    n, p = 12, 2
+    """c2 (32^3 elements, p = 2, u_A): tau in {1e-2, 5e-3, 2.5e-3}, compared at the common time
+    t = 0.25 (steps 25, 50, 100); self-convergence order in [1.8, 2.2] for E and for H."""
+    n, p = 32, 2
     runs = [_run_uA(n, p, tau, st).get_fields() for tau, st in [(1e-2, 25), (5e-3, 50), (2.5e-3, 100)]]
     for grp in (slice(0, 3), slice(3, 6)):
         d1 = np.sqrt(sum(np.sum((a - b) ** 2) for a, b in zip(runs[0][grp], runs[1][grp])))
@@ -413,14 +444,37 @@ def test_P4_temporal_order_c2_taus():
 
 # ---------------------------------------------------------------------------
 # P5: stability (CLAIM-2)
+#
+# Finding (recorded in DESIGN.md §3): the M-norm energy u^T M u is NOT the quantity
+# these ADI schemes conserve.  The exact-Schur Peaceman-Rachford control (first-order
+# (E, H) form of scheme1a-scheme1d with the same Galerkin blocks, tests/dense_ref.py)
+# conserves Et(u) = u^T M u + ||T2 u||^2_{M^-1} (T2 = the explicit curl operator of
+# substep 1), so even it lets u^T M u rise up to Et(0) -- for u_A that is
+# 1 + pi^2 tau^2 / 4 (1.0247 at tau = 1/10, 3.47 at tau = 1, 248 at tau = 10).  The
+# paper's scheme replaces the exact Schur complement by the stiffness K (discrete1/3),
+# a PSD perturbation that keeps rho(G) = 1 but makes G non-normal: transient growth
+# sup_n ||G^n||_M > 1, bounded (power-bounded), no secular growth.  SURVEY's P5(ii)
+# "max E(n) <= 1.01 E(0)" therefore cannot hold at tau >= 1/10; the pins below
+# are the properties that do hold, each checked against an independent computation.
 # ---------------------------------------------------------------------------
+def _masks(N):
+    I = np.arange(N)
+    inner = (I >= 1) & (I <= N - 2)
+    out = []
+    for d in range(3):
+        m = [np.ones(N, bool) if ax == d else inner for ax in range(3)]
+        out.append(np.kron(np.kron(m[2], m[1]), m[0]).astype(bool))
+    return out + [np.ones(N ** 3, bool)] * 3
+
+
 def _amplification(n, p, tau, eps_tf=None):
+    """Brute-force amplification matrix of one oracle step over the free coefficients
+    (E on their PEC active sets, H everywhere): column j = step(e_j)."""
     P = oracle.Patch(n, p, tau)
     if eps_tf is not None:
         P.set_materials_tf(eps_tf)
     N, U = P.N, P.N ** 3
-    D = DenseMaxwell(n, p, tau)
-    masks = [D.active(d) for d in range(3)] + [np.ones(U, bool)] * 3
+    masks = _masks(N)
     idx = [(c, i) for c in range(6) for i in np.nonzero(masks[c])[0]]
     G = np.zeros((len(idx), len(idx)))
     for col, (c, i) in enumerate(idx):
@@ -429,64 +483,140 @@ def _amplification(n, p, tau, eps_tf=None):
         P.set_fields(f)
         P.step(1)
         out = P.get_fields()
-        G[:, col] = [out[cc][ii] for cc, ii in idx]
+        G[:, col] = np.concatenate([out[cc][masks[cc]] for cc in range(6)])
     return G
 
 
-@pytest.mark.parametrize("p", [1, 2])
-@pytest.mark.parametrize("tau", [1e-3, 1e-1, 1.0, 1e3])
-def test_P5_spectral_radius(p, tau):
-    G = _amplification(2, p, tau)
+@pytest.mark.parametrize("n,p", [(3, 1), (3, 2), (3, 3), (4, 2)])
+@pytest.mark.parametrize("tau", [1e-1, 10.0, 1e3])
+def test_P5_pr_control_conserves_energy(n, p, tau):
+    """Control for P5: the exact-Schur Peaceman-Rachford scheme built
+    from the dense weak-form blocks conserves Et to rounding -- every curl block is skew
+    (C1' = -C1^T, C2' = -C2^T under PEC, D1) and every sign of scheme1a-1d / D2 is right.
+    Negative control: flipping the sign of one H-equation block (a D2-type error) breaks it."""
+    D = DenseMaxwell(n, p, tau)
+    f = workloads.random_fields(n + p, 3)
+    _, _, Et = D.step_pr(f[:3], f[3:], tau / 2, tau / 2, steps=3)
+    drift = np.abs(np.diff(Et)) / np.asarray(Et[:-1])
+    assert drift.max() <= 1e-12, drift
+    masks, off, Mb, T1, T2 = D.pr_operators(np.full(D.U, tau / 2), np.full(D.U, tau / 2))
+    u = np.concatenate([x[m] for x, m in zip(f, masks)])
+    bad = T2.copy()
+    bad[off[3]:off[4], :off[3]] *= -1.0  # H1 row of -b C1' E with the wrong sign
+    L1, R1, L2, R2 = Mb - T1, Mb + bad, Mb - bad, Mb + T1
+    e0 = float((L2 @ u) @ np.linalg.solve(Mb, L2 @ u))
+    u1 = np.linalg.solve(L2, R2 @ np.linalg.solve(L1, R1 @ u))
+    e1 = float((L2 @ u1) @ np.linalg.solve(Mb, L2 @ u1))
+    assert abs(e1 - e0) / e0 >= 1e-6
+
+
+_RHO_CASES = [(3, 1, t) for t in (1e-3, 1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3)] + \
+             [(3, 2, t) for t in (1e-3, 1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3)] + \
+             [(4, 1, t) for t in (1e-3, 1e-1, 10.0, 1e3)]
+_RHO_SLOW = [(3, 3, t) for t in (1e-3, 1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3)] + \
+            [(4, 2, t) for t in (1e-3, 1e-2, 1e-1, 1.0, 10.0, 1e2, 1e3)] + \
+            [(4, 1, t) for t in (1e-2, 1.0, 1e2)] + [(4, 3, t) for t in (1e-3, 1.0, 1e3)]
+
+
+@pytest.mark.parametrize("n,p,tau", _RHO_CASES + [pytest.param(*c, marks=pytest.mark.slow) for c in _RHO_SLOW])
+def test_P5_spectral_radius(n, p, tau):
+    """P5(i): rho(G) <= 1 + 1e-12 on 3^3 and 4^3 elements, p = 1..3, tau = 1e-3 .. 1e3
+    (eps = mu = 1): the paper's unconditional stability in the spectral sense.
+    The eigenvalue 1 belongs to the discrete gradients (curl-free E, H), which every step
+    leaves unchanged."""
+    G = _amplification(n, p, tau)
     rho = np.abs(np.linalg.eigvals(G)).max()
     assert rho <= 1 + 1e-12, rho
 
 
+def _mass_sqrt(n, p):
+    D = DenseMaxwell(n, p, 1.0)
+    masks, _, Mb, _, _ = D.pr_operators(np.zeros(D.U), np.zeros(D.U))
+    w, V = np.linalg.eigh(Mb)
+    return (V * np.sqrt(w)) @ V.T, (V / np.sqrt(w)) @ V.T
+
+
 @pytest.mark.slow
-def test_P5_spectral_radius_p3_3cubed():
-    for tau in [1e-2, 1.0, 1e2]:
-        rho = np.abs(np.linalg.eigvals(_amplification(3, 3, tau))).max()
-        assert rho <= 1 + 1e-12, (tau, rho)
+@pytest.mark.parametrize("p", [1, 2])
+@pytest.mark.parametrize("tau", [1.0, 10.0, 1e3])
+def test_P5_power_bounded(p, tau):
+    """P5(i'): no secular growth: ||G^n||_M (n up to 4096, by repeated squaring) levels off --
+    the largest value over n in [512, 4096] does not exceed the largest over n <= 256 by more
+    than 2%.  (A Jordan block at |lambda| = 1 or a rho slightly above 1 would grow ~n or
+    exponentially.)  The transient itself is large: G is non-normal (see the finding above);
+    on 3^3, p = 2 sup_n ||G^n||_M is ~1.07 / 5.8 / 116 at tau = 1/10, 1, 10."""
+    n = 3
+    G = _amplification(n, p, tau)
+    Mh, Mih = _mass_sqrt(n, p)
+    norms = {}
+    X = np.eye(len(G))
+    for k in range(1, 17):
+        X = G @ X
+        norms[k] = np.linalg.norm(Mh @ X @ Mih, 2)
+    X = np.linalg.matrix_power(G, 16)
+    k = 16
+    while k < 4096:
+        X = X @ X
+        k *= 2
+        norms[k] = np.linalg.norm(Mh @ X @ Mih, 2)
+    early = max(v for kk, v in norms.items() if kk <= 256)
+    late = max(v for kk, v in norms.items() if kk >= 512)
+    assert late <= 1.02 * early, (early, late, norms)
+    assert np.isfinite(late)
 
 
-def _energy(P, M, fs):
+def _mass_energy(M, fs):
     e = 0.0
     for f in fs:
-        u = f.reshape(P.N, P.N, P.N)  # [k, j, i]
+        N = M.shape[0]
+        u = f.reshape(N, N, N)  # [k, j, i]
         Mu = np.einsum("ai,bj,ck,kji->cba", M, M, M, u)
-        e += 0.5 * float(np.sum(u * Mu))
+        e += float(np.sum(u * Mu))
     return e
 
 
-def test_P5_energy_tau_tenth():
-    """S:322 reading: u_A, tau = 1/10 over [0,1]: the M-norm energy stays within
-    2% of E(0).  (The paper's scheme is not M-energy conserving -- its implicit
-    K-term is not the exact Schur complement, SURVEY §A.3 -- so a small
-    oscillation, 1.2% here, is expected; growth is not.)"""
-    P = oracle.Patch(8, 2, 0.1)
+@pytest.mark.parametrize("tau,steps", [(0.1, 10), pytest.param(1.0, 10000, marks=pytest.mark.slow),
+                                       pytest.param(10.0, 10000, marks=pytest.mark.slow)])
+def test_P5_energy_uA_bounded(tau, steps):
+    """P5(ii) as it holds: 8^3, p = 2, u_A (eps = mu = 1).  The M-energy u^T M u of the oracle's
+    steps stays below Et(u^0), the quantity the exact-Schur PR control conserves, evaluated on
+    the initial data by the independent dense blocks (measured max u^T M u / u0^T M u0: 1.0120
+    at tau = 1/10 (10 steps), 2.912 at tau = 1, 245.3 at tau = 10 against Et(0) / u0^T M u0 =
+    1.0247, 3.467, 247.7); and there is no secular growth (10^4 steps: the second half's
+    maximum does not exceed the first half's)."""
+    n, p = 8, 2
+    P = oracle.Patch(n, p, tau)
     P.project_uA(0.0)
+    f0 = P.get_fields()
     M, _, _ = P.matrices()
-    E0 = _energy(P, M, P.get_fields())
-    for _ in range(10):
-        P.step(1)
-        assert _energy(P, M, P.get_fields()) <= 1.02 * E0
-
-
-@pytest.mark.slow
-@pytest.mark.parametrize("tau", [1.0, 10.0])
-def test_P5_long_run_bounded(tau):
-    """8^3, p=2, u_A, tau in {1, 10}, 1000 steps: no secular growth (stability =
-    bounded powers of the amplification matrix; rho(G) = 1 by test_P5_spectral_radius).
-    The energy oscillates quasi-periodically (non-normal G); the second half of
-    the run must not exceed the first half's maximum by more than 10%."""
-    P = oracle.Patch(8, 2, tau)
-    P.project_uA(0.0)
-    M, _, _ = P.matrices()
+    D = DenseMaxwell(n, p, tau)
+    em0, et0 = D.pr_energy(f0[:3], f0[3:], tau / 2, tau / 2)
+    assert abs(_mass_energy(M, f0) - em0) <= 1e-12 * em0  # the two mass matrices agree
+    every = 1 if steps <= 100 else 10
     tr = []
-    for _ in range(40):
-        P.step(25)
-        tr.append(_energy(P, M, P.get_fields()))
-    assert all(np.isfinite(tr))
-    assert max(tr[20:]) <= 1.1 * max(tr[:20]), (max(tr[:20]), max(tr[20:]))
+    for _ in range(steps // every):
+        P.step(every)
+        tr.append(_mass_energy(M, P.get_fields()))
+    tr = np.array(tr)
+    assert tr.max() <= et0 * (1 + 1e-12), (tr.max() / em0, et0 / em0)
+    if steps >= 1000:
+        h = len(tr) // 2
+        assert tr[h:].max() <= tr[:h].max() * (1 + 1e-9), (tr[:h].max() / em0, tr[h:].max() / em0)
+
+
+@pytest.mark.parametrize("tau", [0.01, 0.1, 10.0])
+def test_P5_random_material_report(tau):
+    """P5(iii), reported not asserted as stable: i.i.d. per-test-function eps in [1, 80] (3^3,
+    p = 2).  Row scaling makes the mass non-symmetric and the energy argument fails (SURVEY
+    §A.3); measured rho(G) - 1 is ~1e-4..9e-4 at tau = 0.01..0.1 (a finding: slow growth) and
+    at rounding level for tau >= 1.  The assertion only brackets what was measured."""
+    worst = 0.0
+    for seed in range(2):
+        eps = workloads.random_tf(5, 70 + seed, 1.0, 80.0)
+        rho = np.abs(np.linalg.eigvals(_amplification(3, 2, tau, eps))).max()
+        worst = max(worst, rho)
+    print(f"P5(iii) tau={tau}: max rho(G) - 1 = {worst - 1:.3e}")
+    assert worst <= 1.01, worst
 
 
 # ---------------------------------------------------------------------------
