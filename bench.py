@@ -235,11 +235,12 @@ def parity_probe(cfg, n_small: int = 16, steps: int = 2):
     return {"max_rel_l2": max(errs), "case": f"{cfg['name']} recipe at n={n}, {steps} steps, GPU vs oracle"}
 
 
-def dist_init(force: bool = False):
-    """torch.distributed over NCCL when launched by torchrun with N > 1 (or forced, e.g.
-    --slabs under torchrun with one process)."""
+def dist_init():
+    """torch.distributed over NCCL when launched by torchrun with N > 1 (plumbing only: the id
+    broadcast and the barriers / max-over-ranks of the timing; the step's exchanges are the
+    library's own NCCL communicator)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws > 1 or (force and "MASTER_ADDR" in os.environ):
+    if ws > 1:
         import torch.distributed as dist
 
         import torch
@@ -288,10 +289,11 @@ def run_reference(args, cfg):
 
 def parallelism_label(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
-    if ws == 1 and not args.slabs:
+    if ws == 1:
         return "single GPU, whole patch, CUDA graph per step"
-    return (f"z-slab decomposition over {ws} rank(s) (one process per GPU): NCCL halo exchange before the "
-            "RHS, all-to-all z<->y transposes around z-sweeps (paper_2103_06998_b200.dist)")
+    return (f"z-slab decomposition over {ws} GPUs (one process per GPU), the library's distributed adi_step: "
+            "NCCL halo exchange before the RHS stencils, batched all-to-all z<->y transposes around the z sweeps, "
+            "one CUDA graph per step")
 
 
 def config_dict(cfg, args):
@@ -341,49 +343,46 @@ class _Whole:
         self.G.close()
 
 
-class _Slabs:
-    """N > 1 GPUs: this rank's z-slab (paper_2103_06998_b200.dist), exchanges over NCCL."""
+class _Dist:
+    """N > 1 GPUs: this rank's z-slab patch; the library runs the distributed schedule itself
+    (adi_step over NCCL: halo exchanges and batched z<->y transposes, one CUDA graph per step)."""
 
     def __init__(self, cfg, local, seed):
         import torch
 
-        from paper_2103_06998_b200.dist import DistPatch
+        from paper_2103_06998_b200.dist import create_patch
 
         n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
         self.N = N = n + p
-        self.D = DistPatch(n, p, tau, device=local)
-        self.D.set_materials(workloads.element_eps(n, cfg["material"]))
+        self.G = create_patch(n, p, tau, device=local)
+        _, k0, k1 = self.G.layout()
+        self.nz = k1 - k0
+        self.G.set_materials(workloads.element_eps(n, cfg["material"]))
         rng = np.random.default_rng(seed)
-        nz = self.D.nz
-        self.fields = [torch.from_numpy(rng.uniform(-1.0, 1.0, size=(nz, N, N))).pin_memory() for _ in range(6)]
-        self.D.set_fields(self.fields)
-        self.stream_handle = self.D.stream.cuda_stream
-        self.local_bytes = 6 * nz * N * N * 8
+        self.fields = [torch.from_numpy(rng.uniform(-1.0, 1.0, size=self.nz * N * N)).pin_memory() for _ in range(6)]
+        self.G.set_fields(self.fields)
+        self.stream_handle = self.G.stream
+        self.local_bytes = 6 * self.nz * N * N * 8
 
     def step(self, k):
-        self.D.step(k)
+        self.G.step(k)
 
     def timing(self, on):
-        self.D.B.set_timing(on)
+        self.G.set_timing(on)
 
     def report(self):
-        return self.D.B.timing_report()
+        return self.G.timing_report()
 
     def e2e(self, out_host):
-        self.D.set_fields(self.fields)
-        self.D.step(self.k_e2e)
-        for o, f in zip(out_host, self.D.get_fields()):
-            o.copy_(f.view(-1))
+        self.G.set_fields(self.fields)
+        self.G.step(self.k_e2e)
+        self.G.get_fields(out_host)
 
     def launches_per_step(self):
-        self.D.B.set_timing(True)
-        self.D.step(1)
-        rep = self.D.B.timing_report()
-        self.D.B.set_timing(False)
-        return sum(v[1] for v in rep.values())
+        return self.G.launches_per_step
 
     def close(self):
-        pass
+        self.G.close()
 
 
 def run_ours(args, cfg):
@@ -391,14 +390,14 @@ def run_ours(args, cfg):
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist, rank, ws = dist_init(force=args.slabs)
+    dist, rank, ws = dist_init()
     import paper_2103_06998_b200 as adi
 
     adi.build()
     n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
     N = n + p
     U = N ** 3
-    S = (_Whole if ws == 1 and not args.slabs else _Slabs)(cfg, local, 1000 + rank)
+    S = (_Whole if ws == 1 else _Dist)(cfg, local, 1000 + rank)
     S.step(args.warmup)
     torch.cuda.synchronize()
     # ---------------- timed region (device-resident state) ----------------
@@ -538,8 +537,6 @@ def main():
     ap.add_argument("--oracle-steps", type=int, default=2,
                     help="steps per timed oracle region (5 regions, median)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--slabs", action="store_true",
-                    help="use the slab-decomposed path (paper_2103_06998_b200.dist) even on one GPU")
     args = ap.parse_args()
     cfg = dict(workloads.CONFIGS[args.config])
     cfg["name"] = args.config

@@ -53,7 +53,7 @@ typedef enum {
   ADI_ERR_STATE = 2,    /* e.g. adi_step before adi_set_fields */
   ADI_ERR_SINGULAR = 3, /* a pivot |u_kk| < 1e-14 max|row| in a factorisation */
   ADI_ERR_CUDA = 4,     /* CUDA runtime error: patch poisoned */
-  ADI_ERR_NCCL = 5,     /* reserved for the distributed path: patch poisoned */
+  ADI_ERR_NCCL = 5,     /* NCCL / exchange failure in distributed mode: patch poisoned */
   ADI_ERR_OOM = 6       /* device allocation failed */
 } adi_status;
 
@@ -66,16 +66,42 @@ typedef struct {
   int32_t bc;      /* adi_bc; ADI_BC_PEC (D1) is the paper's Eq. (1) E x n = 0 */
   int32_t device;  /* CUDA device ordinal */
   int32_t rank;    /* this process's rank (0 for a single GPU) */
-  int32_t nranks;  /* 1: whole patch on this device; > 1: box-mode patch (see adi_box_*) */
+  int32_t nranks;  /* 1: whole patch on this device; > 1: one z-slab per rank (see below) */
   void* stream;    /* cudaStream_t to run on; NULL = a library-owned non-blocking stream */
+  /* Distributed mode (nranks > 1).  Exactly one transport, or neither:
+   *   nccl_id:  the 128-byte ncclUniqueId from adi_nccl_unique_id() on rank 0, broadcast to every
+   *             rank (e.g. torch.distributed.broadcast_object_list); the patch creates and owns an
+   *             NCCL communicator of nranks ranks, one process (or thread) and one GPU per rank.
+   *             NCCL is loaded at run time (dlopen "libnccl.so.2"); failures are ADI_ERR_NCCL.
+   *   loopback: a group from adi_loopback_create(nranks) shared by nranks patches of ONE process,
+   *             each driven by its own host thread (tests / single-device runs): exchanges are
+   *             device copies between the patches' buffers ordered by a host barrier (no kernel ever
+   *             waits on another rank's kernel).
+   *   neither:  "box mode": the patch holds only the 1D operators and the adi_box_* entry points
+   *             (the caller owns the slabs and the schedule, e.g. paper_2103_06998_b200.dist). */
+  const void* nccl_id;
+  void* loopback;
 } adi_config;
 
 /* Create a patch: assembles the 1D Galerkin matrices M, S, A (B = A^T) by
  * Gauss quadrature q = p+1 (D4, D11), factors the constant mass sweeps,
- * allocates 14 N^3 device arrays + sweep scratch, sets eps = mu = 1.
- * ADI_ERR_ARG: n < 1, p outside 1..5, tau <= 0 / non-finite, bc invalid,
- * nranks != 1.  ADI_ERR_OOM: device allocation failed.  *out = NULL on error. */
+ * allocates the field, scratch and material arrays (whole patch: N^3 each; distributed:
+ * the rank's z-slab with p halo planes per side, and y-slab work buffers), sets eps = mu = 1.
+ * Distributed mode is collective: every rank must call adi_create (and later every set_* and
+ * adi_step) with the same arguments except rank.
+ * ADI_ERR_ARG: n < 1, p outside 1..5, tau <= 0 / non-finite, bc invalid, rank outside
+ * [0, nranks), nranks > N, both nccl_id and loopback given.  ADI_ERR_OOM: device allocation
+ * failed.  ADI_ERR_NCCL: communicator creation failed.  *out = NULL on error. */
 adi_status adi_create(const adi_config* cfg, adi_patch* out);
+
+/* Rank 0 of a distributed run: writes a fresh ncclUniqueId (128 bytes) to id_out, to be
+ * broadcast to all ranks and passed as adi_config.nccl_id.  ADI_ERR_NCCL if NCCL is unavailable. */
+adi_status adi_nccl_unique_id(void* id_out);
+
+/* In-process exchange group for nranks patches driven by nranks host threads (loopback
+ * transport).  The group must outlive its patches.  ADI_ERR_ARG for nranks < 1. */
+adi_status adi_loopback_create(int32_t nranks, void** group_out);
+void adi_loopback_destroy(void* group);
 
 /* Free all device state. NULL-safe. */
 void adi_destroy(adi_patch patch);
@@ -92,15 +118,18 @@ adi_status adi_set_tau(adi_patch patch, double tau);
  * ADI_ERR_ARG if any value is <= 0 or non-finite (eps, mu >= delta > 0). */
 adi_status adi_set_materials(adi_patch patch, const double* eps_elem, const double* mu_elem);
 
-/* Per-test-function materials given directly (N^3 each; mu NULL => 1). */
+/* Per-test-function materials given directly (N^3 each; mu NULL => 1).
+ * Distributed mode: material and source arrays are GLOBAL (the whole patch, given on every
+ * rank); each rank keeps its slabs of them. */
 adi_status adi_set_materials_tf(adi_patch patch, const double* eps_tf, const double* mu_tf);
 
-/* Set the six coefficient fields (N^3 each).  PEC-eliminated E entries are
- * forced to 0 (D1).  Resets nothing else (step index is kept). */
+/* Set the six coefficient fields: whole patch N^3 each; distributed: the rank's local z-slab,
+ * N x N x (k1 - k0) from adi_layout (x fastest, planes k0..k1-1 of the global grid).
+ * PEC-eliminated E entries are forced to 0 (D1).  Resets nothing else (step index is kept). */
 adi_status adi_set_fields(adi_patch patch, const double* const f[6]);
 
-/* Read the six fields into caller buffers (N^3 each; NULL entries skipped).
- * Synchronises the patch stream. */
+/* Read the six fields into caller buffers (same extents as adi_set_fields; NULL entries
+ * skipped).  Synchronises the patch stream. */
 adi_status adi_get_fields(adi_patch patch, double* const f[6]);
 
 /* Sources (D9): in both substeps of step m, R_d -= a (.) signal[m] * load[d],
@@ -114,7 +143,11 @@ adi_status adi_set_point_source(adi_patch patch, int32_t comp, double xs, double
                                 const double* signal, int64_t nsig);
 
 /* Advance k >= 0 full time steps.  Asynchronous on the patch stream (the first
- * call for a given patch state captures the step into a CUDA graph).
+ * call for a given patch state captures the step into a CUDA graph; distributed NCCL patches
+ * capture the NCCL exchanges into the same graph, loopback patches run eagerly).
+ * Distributed mode (collective): per substep a p-plane halo exchange of the six fields before
+ * the RHS stencils, x / y sweeps on the z-slab, and every z sweep on y-slabs between batched
+ * all-to-all transposes (one exchange per stage for all components); SURVEY §8(e).
  * ADI_ERR_STATE before adi_set_fields. */
 adi_status adi_step(adi_patch patch, int64_t k);
 

@@ -22,7 +22,7 @@ _ROOT = os.path.dirname(_HERE)
 # ADI_LIB selects another build of the library (tuning experiments); default: the in-tree build
 LIB_PATH = os.environ.get("ADI_LIB") or os.path.join(_HERE, "lib", "libadimaxwell.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh", "sweep_tw.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh", "sweep_tw.cuh", "sweep_tma.cuh", "sweep_res.cuh")] + [
     os.path.join(_ROOT, "include", "adi_maxwell.h")]
 DEGREES = (1, 2, 3, 4, 5)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -40,11 +40,13 @@ EXPORTS = [
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
     "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA", "adi_divergence",
+    "adi_nccl_unique_id", "adi_loopback_create", "adi_loopback_destroy",
 ]
 
 
 
-def build(force: bool = False, verbose: bool = False, lib_path: str | None = None, extra_flags=()) -> str:
+def build(force: bool = False, verbose: bool = False, lib_path: str | None = None, extra_flags=(),
+          degrees=DEGREES) -> str:
     """Compile libadimaxwell.so in-tree for sm_100a (nvcc; no GPU needed).
 
     One object per B-spline degree (csrc/degree.cu with -DADI_P=p) plus the host
@@ -57,8 +59,9 @@ def build(force: bool = False, verbose: bool = False, lib_path: str | None = Non
     objdir = os.path.join(os.path.dirname(lib_path), "obj")
     os.makedirs(objdir, exist_ok=True)
     jobs = [(os.path.join(objdir, "adi_maxwell.o"), [os.path.join(CSRC, "adi_maxwell.cu")])]
-    for p in DEGREES:
-        jobs.append((os.path.join(objdir, f"degree_p{p}.o"), [f"-DADI_P={p}", os.path.join(CSRC, "degree.cu")]))
+    for p in DEGREES:  # degrees not in `degrees` (tuning builds) compile as stubs
+        stub = [] if p in degrees else ["-DADI_STUB"]
+        jobs.append((os.path.join(objdir, f"degree_p{p}.o"), [f"-DADI_P={p}", *stub, os.path.join(CSRC, "degree.cu")]))
     procs = []
     for obj, args in jobs:
         cmd = ["nvcc", *NVCC_FLAGS, *extra_flags, "-c", "-o", obj, *args]
@@ -69,7 +72,7 @@ def build(force: bool = False, verbose: bool = False, lib_path: str | None = Non
     if bad:
         raise RuntimeError("nvcc failed: " + " | ".join(" ".join(c) for c in bad))
     tmp = lib_path + ".tmp"
-    cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *[o for o, _ in jobs]]
+    cmd = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *[o for o, _ in jobs], "-ldl"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
@@ -85,8 +88,10 @@ class SweepJob(C.Structure):
 
 
 class AdiConfig(C.Structure):
+    """adi_config (include/adi_maxwell.h)."""
     _fields_ = [("n", C.c_int32), ("p", C.c_int32), ("tau", C.c_double), ("bc", C.c_int32),
-                ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("stream", C.c_void_p)]
+                ("device", C.c_int32), ("rank", C.c_int32), ("nranks", C.c_int32), ("stream", C.c_void_p),
+                ("nccl_id", C.c_void_p), ("loopback", C.c_void_p)]
 
 
 _lib = None
@@ -147,6 +152,10 @@ def lib():
             L.adi_project_weighted.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
             L.adi_errors_uA.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
             L.adi_divergence.argtypes = [C.c_void_p, C.c_void_p]
+            L.adi_nccl_unique_id.argtypes = [C.c_void_p]
+            L.adi_loopback_create.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
+            L.adi_loopback_destroy.argtypes = [C.c_void_p]
+            L.adi_loopback_destroy.restype = None
             _lib = L
         return _lib
 
@@ -194,14 +203,62 @@ def _ptr_array(objs, count: int | None = None, what: str = "array"):
     return arr
 
 
+def nccl_unique_id() -> bytes:
+    """Rank 0 of a distributed run: a fresh 128-byte ncclUniqueId (adi_nccl_unique_id), to be
+    broadcast to every rank and passed to Patch(..., nccl_id=...)."""
+    L = lib()
+    buf = C.create_string_buffer(128)
+    st = L.adi_nccl_unique_id(buf)
+    if st != ADI_OK:
+        raise AdiError(st, L.adi_last_error().decode())
+    return buf.raw
+
+
+class Loopback:
+    """In-process exchange group of `nranks` patches driven by `nranks` host threads on one
+    device (adi_loopback_create): the library's distributed schedule without NCCL."""
+
+    def __init__(self, nranks: int):
+        self._L = lib()
+        h = C.c_void_p()
+        st = self._L.adi_loopback_create(int(nranks), C.byref(h))
+        if st != ADI_OK:
+            raise AdiError(st, self._L.adi_last_error().decode())
+        self.h = h
+        self.nranks = int(nranks)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.adi_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Patch:
-    """One n x n x n patch on one B200 (device memory owned by the library)."""
+    """One n x n x n patch (or, distributed, this rank's z-slab of it) on one B200; device
+    memory owned by the library.  nranks > 1 with nccl_id (bytes from nccl_unique_id()) or
+    loopback (a Loopback group) runs the library's distributed schedule; nranks > 1 with
+    neither is a box-mode patch (adi_box_* only)."""
 
     def __init__(self, n: int, p: int, tau: float, bc: int = ADI_BC_PEC, device: int = 0, rank: int = 0,
-                 nranks: int = 1, stream: int | None = None):
+                 nranks: int = 1, stream: int | None = None, nccl_id: bytes | None = None,
+                 loopback: "Loopback | None" = None):
         L = lib()
         self._L = L
-        cfg = AdiConfig(int(n), int(p), float(tau), int(bc), int(device), int(rank), int(nranks), stream)
+        self._id = None
+        if nccl_id is not None:
+            if len(nccl_id) != 128:
+                raise ValueError("nccl_id: need the 128-byte ncclUniqueId")
+            self._id = C.create_string_buffer(bytes(nccl_id), 128)
+        self._loop = loopback
+        cfg = AdiConfig(int(n), int(p), float(tau), int(bc), int(device), int(rank), int(nranks), stream,
+                        C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                        loopback.h if loopback is not None else None)
         h = C.c_void_p()
         self._check(L.adi_create(C.byref(cfg), C.byref(h)))
         self.h = h

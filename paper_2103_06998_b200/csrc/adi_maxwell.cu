@@ -9,8 +9,14 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -150,6 +156,7 @@ void assemble_1d(const Space1D& sp, std::vector<double>& M, std::vector<double>&
 // ---------------------------------------------------------------------------
 // Patch
 // ---------------------------------------------------------------------------
+struct Transport;  // distributed exchanges (NCCL or in-process loopback), below
 struct adi_patch_s {
   adi_config cfg{};
   int n = 0, p = 0, N = 0, W = 0;
@@ -208,6 +215,35 @@ struct adi_patch_s {
   int nsm = 148;
   int sw_bps[3] = {0, 0, 0};  // ADI_SW_BPS_MASS / _MOD / _DER: blocks per SM cap (0 = occupancy)
   int use_tma = 0;   // RHS halo planes by TMA (N even, encoder available; ADI_RHS_CPA=1 disables)
+  // TMA-staged sweeps (sweep_tma.cuh) where the layout allows, bit m = mode m (ADI_SW_TMA).  Default:
+  // mass and derivative projection (measured faster at c5); the row-modified sweep stays on the
+  // cp.async kernel, whose pass-2 working set (f, c, pivots) fits L2 better at its warp count.
+  int use_st = (1 << 0) | (1 << 2);
+  int st_grid[3] = {0, 0, 0};  // blocks of the TMA-staged sweep per mode (one per SM)
+  int use_res = 0;   // fiber-resident two-segment sweeps (sweep_res.cuh), opt-in (ADI_SW_RES=1): measured slower at c5
+  bool res_ok = false;
+  // ---- distributed (slab) mode: nranks > 1 with a transport ----
+  int slab = 0;                 // 1: this patch is rank `rank` of a slab-decomposed run
+  int nrk = 1, rank = 0;         // ranks of the run, this rank
+  int k0 = 0, k1 = 0, nz = 0;   // own z-planes [k0, k1) (fields stored with p halo planes per side)
+  int j0 = 0, j1 = 0, ny = 0;   // own y-rows [j0, j1) of the y-slab layout (z sweeps)
+  int64_t UL = 0, UH = 0, UY = 0;  // entries of a z-slab, a halo'd z-slab, a y-slab
+  double* Y[6] = {};            // y-slab work buffers (transposed fields of the z sweeps)
+  double* cy = nullptr;         // c in the y-slab layout
+  double* xbuf[2] = {};         // pack / unpack buffers of the transposes (3 z-slabs each)
+  Transport* tr = nullptr;
+};
+
+// Exchanges of the distributed (slab) mode; implementations below (NCCL, in-process loopback)
+struct Transport {
+  virtual ~Transport() {}
+  virtual bool capturable() const = 0;
+  // p halo planes of nf halo'd z-slab fields from / to the z-neighbours
+  virtual adi_status halo(adi_patch P, double* const* f, int nf) = 0;
+  // inner planes of the halo'd z-slabs src[q] -> y-slabs dst[q] (nf <= 3 fields, one exchange)
+  virtual adi_status z2y(adi_patch P, double* const* src, double* const* dst, int nf) = 0;
+  // y-slabs src[q] -> inner planes of the halo'd z-slabs dst[q]
+  virtual adi_status y2z(adi_patch P, double* const* src, double* const* dst, int nf) = 0;
 };
 
 namespace {
@@ -406,9 +442,12 @@ struct SweepReq {
   const double* base = nullptr;  // derivative projection: out = base + coef M^{-1} A in
   double coef = 0.0;
   int64_t dims[3] = {0, 0, 0};   // box extents (x fastest); 0 = the whole N^3 patch
+  const double* c = nullptr;     // modified: per-row c in the job's layout (nullptr: the patch's)
 };
 
-adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_fibers = 32) {
+// tiles: legacy kernels flatten the fibers into tiles of tile_fibers; the TMA-staged kernel
+// (st_tiles) uses boxes of 32 consecutive fibers along the fastest fiber index per row.
+adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_fibers = 32, int st_tiles = 0) {
   adi::SweepBatch B{};
   B.N = P->N;
   B.njobs = nreq;
@@ -420,10 +459,15 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_
     const int ax = req[j].axis;
     const int64_t nfib = (int64_t)J.dims[(ax + 1) % 3] * J.dims[(ax + 2) % 3];
     J.tile0 = (int)tiles;
-    tiles += (nfib + tile_fibers - 1) / tile_fibers;
+    if (st_tiles) {  // boxes of st_tiles consecutive fibers along the fastest fiber index
+      const int64_t nf = ax == 0 ? J.dims[1] : J.dims[0];
+      tiles += (nf + st_tiles - 1) / st_tiles * (nfib / nf);
+    } else {
+      tiles += (nfib + tile_fibers - 1) / tile_fibers;
+    }
     J.in = req[j].in;
     J.out = req[j].out;
-    J.c = P->c;
+    J.c = req[j].c ? req[j].c : P->c;
     J.iu = req[j].iu;
     J.base = req[j].base;
     J.coef = req[j].coef;
@@ -464,12 +508,111 @@ bool twisted(adi_patch P, const SweepReq* req, int nreq, int mode) {
   return true;
 }
 
+// 3D map of a sweep job array (dims x fastest) with the chunk box of sweep_tma.cuh:
+// x sweeps {16, 32, 1} with the 128-byte swizzle, y sweeps {32, 16, 1}, z sweeps {32, 1, 16}.
+bool make_sweep_map(CUtensorMap* m, const double* ptr, const int dims[3], int axis) {
+  auto enc = tma_encoder();
+  if (!enc || !ptr || (dims[0] & 1) || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  cuuint64_t gd[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)dims[0] * 8, (cuuint64_t)dims[0] * dims[1] * 8};
+  cuuint32_t box[3];
+  if (axis == 0) box[0] = adi::ST_CH, box[1] = 32, box[2] = 1;
+  else if (axis == 1) box[0] = 32, box[1] = adi::ST_CH, box[2] = 1;
+  else box[0] = 32, box[1] = 1, box[2] = adi::ST_CH;
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), gd, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, axis == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// Tensor maps of the TMA-staged sweep (sweep_tma.cuh) for every array of every job of B;
+// false if some array cannot be mapped (odd x extent, misaligned pointer, no encoder).
+bool sweep_tma_maps(adi_patch P, const adi::SweepBatch& B, int mode, adi::SweepTmaMaps& maps) {
+  if (!(P->use_st & (1 << mode)) || P->st_grid[mode] < 1) return false;
+  memset(&maps, 0, sizeof maps);
+  for (int j = 0; j < B.njobs; j++) {
+    const adi::SweepJob& J = B.job[j];
+    if (mode == adi::SW_MOD && (!J.iu || !J.c)) return false;
+    const double* aux = mode == adi::SW_MOD ? J.c : mode == adi::SW_DER ? J.base : J.in;
+    const double* piv = mode == adi::SW_MOD ? J.iu : J.in;
+    if (!make_sweep_map(&maps.m[j][0], J.in, J.dims, J.axis) || !make_sweep_map(&maps.m[j][1], aux, J.dims, J.axis) ||
+        !make_sweep_map(&maps.m[j][2], piv, J.dims, J.axis) || !make_sweep_map(&maps.m[j][3], J.out, J.dims, J.axis))
+      return false;
+  }
+  return true;
+}
+
+// 3D map of a job array with the boxes of sweep_res.cuh: y / z sweeps {16 fibers, 64 rows},
+// x sweeps {16 rows, 16 fibers} with the 128-byte swizzle.
+bool make_res_map(CUtensorMap* m, const double* ptr, const int dims[3], int axis) {
+  auto enc = tma_encoder();
+  if (!enc || !ptr || (dims[0] & 1) || (reinterpret_cast<uintptr_t>(ptr) & 15)) return false;
+  cuuint64_t gd[3] = {(cuuint64_t)dims[0], (cuuint64_t)dims[1], (cuuint64_t)dims[2]};
+  cuuint64_t strides[2] = {(cuuint64_t)dims[0] * 8, (cuuint64_t)dims[0] * dims[1] * 8};
+  cuuint32_t box[3];
+  if (axis == 0) box[0] = 16, box[1] = 16, box[2] = 1;
+  else if (axis == 1) box[0] = 16, box[1] = adi::SR_SLOT, box[2] = 1;
+  else box[0] = 16, box[1] = 1, box[2] = adi::SR_SLOT;
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(ptr), gd, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, axis == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// fiber-resident two-segment launch (sweep_res.cuh) of MASS / DER jobs, if possible
+bool launch_sweeps_res(adi_patch P, const SweepReq* req, int nreq, int mode, cudaStream_t st, adi_status& status) {
+  if (!P->use_res || !P->res_ok || (mode != adi::SW_MASS && mode != adi::SW_DER)) return false;
+  const size_t per = adi::sr_warp_bytes(P->N, mode);
+  const int warps = (int)std::min<size_t>(adi::SR_MAXW, (227 * 1024 - 1024) / per);
+  if (warps < 1) return false;
+  adi::SweepBatch B = make_batch(P, req, nreq, 32, 16);
+  adi::SweepResMaps maps;
+  memset(&maps, 0, sizeof maps);
+  for (int j = 0; j < nreq; j++) {
+    const adi::SweepJob& J = B.job[j];
+    if (!P->tw_ok[J.var]) return false;
+    const double* base = mode == adi::SW_DER ? J.base : J.in;
+    if (!make_res_map(&maps.m[j][0], J.in, J.dims, J.axis) || !make_res_map(&maps.m[j][1], base, J.dims, J.axis) ||
+        !make_res_map(&maps.m[j][2], J.out, J.dims, J.axis))
+      return false;
+  }
+  LaunchScope ls(P, mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
+  const int64_t blocks_needed = ((int64_t)B.ntiles + warps - 1) / warps;
+  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->nsm);
+  const size_t smem = (size_t)warps * per + 1024;
+  with_degree(P->p, [&](auto ops) { ops.sweep_res(st, grid, (unsigned)warps, smem, B, maps, mode); });
+  cudaError_t e = cudaGetLastError();
+  status = e == cudaSuccess ? ADI_OK : fail(ADI_ERR_CUDA, "sweep_res launch: %s", cudaGetErrorString(e));
+  return true;
+}
+
 adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode, cudaStream_t st = nullptr,
                          double* ckpt = nullptr) {
+  if (!st) st = P->stream;
+  {
+    adi_status rst = ADI_OK;
+    if (launch_sweeps_res(P, req, nreq, mode, st, rst)) return rst;
+  }
+  if (P->use_st && !(P->use_tw && mode != adi::SW_MOD)) {
+    adi::SweepBatch B = make_batch(P, req, nreq, 32, 32);
+    if (ckpt) B.ckpt = ckpt;
+    adi::SweepTmaMaps maps;
+    if (sweep_tma_maps(P, B, mode, maps)) {
+      B.nck = (P->N + adi::ST_CH - 1) / adi::ST_CH;
+      LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
+      const int warps = adi::st_warps(mode);
+      const int64_t blocks_needed = ((int64_t)B.ntiles + warps - 1) / warps;
+      const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->st_grid[mode]);
+      with_degree(P->p, [&](auto ops) { ops.sweep_tma(st, grid, B, maps, mode); });
+      CUDA_TRY(cudaGetLastError());
+      return ADI_OK;
+    }
+  }
   const bool tw = twisted(P, req, nreq, mode);
   adi::SweepBatch B = make_batch(P, req, nreq, tw ? 16 : 32);
   if (ckpt) B.ckpt = ckpt;
-  if (!st) st = P->stream;
   B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
   LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
   const int64_t warps_needed = B.ntiles;
@@ -492,6 +635,21 @@ adi_status sweep_setup(adi_patch P) {
     if (P->sw_bps[m] > 0) bps = std::min(bps, P->sw_bps[m]), bps_tw = std::min(bps_tw, P->sw_bps[m]);
     P->sw_grid[m] = P->nsm * bps;
     P->sw_grid_tw[m] = P->nsm * bps_tw;
+  }
+  int occ_st[3] = {0, 0, 0};
+  if (P->use_st && tma_encoder()) {
+    e = with_degree(P->p, [&](auto ops) { return ops.sweep_tma_attrs(occ_st); });
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ADI_ERR_CUDA, "TMA sweep kernel attributes: %s", cudaGetErrorString(e));
+    }
+  }
+  for (int m = 0; m < 3; m++) P->st_grid[m] = occ_st[m] >= 1 ? P->nsm : 0;  // one block per SM
+  P->res_ok = false;
+  if (P->use_res && tma_encoder()) {
+    e = with_degree(P->p, [&](auto ops) { return ops.sweep_res_attrs(); });
+    if (e != cudaSuccess) cudaGetLastError();
+    P->res_ok = e == cudaSuccess;
   }
   return ADI_OK;
 }
@@ -637,14 +795,434 @@ adi_status substep(adi_patch P, int s) {
   return ADI_OK;
 }
 
+adi_status dist_substep(adi_patch P, int s);
+
 adi_status full_step(adi_patch P) {
   adi_status st;
-  if ((st = substep(P, 1))) return st;
-  if ((st = substep(P, 2))) return st;
+  if ((st = P->slab ? dist_substep(P, 1) : substep(P, 1))) return st;
+  if ((st = P->slab ? dist_substep(P, 2) : substep(P, 2))) return st;
   {
     LaunchScope ls(P, ADI_K_OTHER);
     adi::increment_kernel<<<1, 1, 0, P->stream>>>(P->d_step);
     CUDA_TRY(cudaGetLastError());
+  }
+  return ADI_OK;
+}
+
+// ===========================================================================
+// Distributed (slab) mode -- SURVEY §8(e).  Rank r of R owns the z-planes
+// [r N / R, (r+1) N / R) of every field (stored with p halo planes on each side,
+// zeros at the patch ends) and the y-rows [r N / R, (r+1) N / R) of the y-slab
+// layout in which its z sweeps run.  Exchanges per substep: a p-plane halo
+// exchange of the six fields before the RHS stencils (the general-mu path also
+// exchanges the new E before the H stencil), and one batched all-to-all
+// transpose z-slab -> y-slab (and back) per sweep stage that has z sweeps.
+// Per-fiber arithmetic is identical to the whole patch: results are independent
+// of R bit for bit.
+// ===========================================================================
+int64_t slab_lo(int N, int R, int r) { return (int64_t)r * N / R; }
+
+// 3D strided box copy on the patch stream (the pack / unpack of the transposes)
+adi_status box_copy(adi_patch P, double* dst, int64_t dx, int64_t dy, int64_t ox, int64_t oy, int64_t oz,
+                    const double* src, int64_t sx, int64_t sy, int64_t px, int64_t py, int64_t pz, int64_t ex,
+                    int64_t ey, int64_t ez) {
+  if (ex * ey * ez == 0) return ADI_OK;
+  adi::copy_box_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(dst, dx, dy, ox, oy, oz, src, sx, sy, px, py, pz, ex, ey, ez);
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
+// ---- NCCL, loaded at run time (no link-time dependency of the library) ----
+struct NcclApi {
+  bool ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);  // the process's NCCL if already loaded (torch)
+    if (!h) {
+      a.why = dlerror() ? "dlopen libnccl.so.2 failed" : "libnccl.so.2 not found";
+      return a;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    a.GetUniqueId = (decltype(a.GetUniqueId))sym("ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))sym("ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");
+    a.GroupStart = (decltype(a.GroupStart))sym("ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
+    a.Send = (decltype(a.Send))sym("ncclSend");
+    a.Recv = (decltype(a.Recv))sym("ncclRecv");
+    a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv &&
+           a.GetErrorString;
+    if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+#define NCCL_TRY(expr)                                                                                  \
+  do {                                                                                                  \
+    ncclResult_t _r = (expr);                                                                           \
+    if (_r != ncclSuccess) return fail(ADI_ERR_NCCL, "%s failed: %s", #expr, nccl_api().GetErrorString(_r)); \
+  } while (0)
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  ~NcclTransport() override {
+    if (comm) nccl_api().CommDestroy(comm);
+  }
+  bool capturable() const override { return true; }
+  adi_status halo(adi_patch P, double* const* f, int nf) override {
+    const NcclApi& A = nccl_api();
+    const int64_t NN = (int64_t)P->N * P->N, pl = (int64_t)P->p * NN;
+    NCCL_TRY(A.GroupStart());
+    for (int q = 0; q < nf; q++) {
+      if (P->rank > 0) {
+        NCCL_TRY(A.Send(f[q] + pl, pl, ncclDouble, P->rank - 1, comm, P->stream));
+        NCCL_TRY(A.Recv(f[q], pl, ncclDouble, P->rank - 1, comm, P->stream));
+      }
+      if (P->rank < P->nrk - 1) {
+        NCCL_TRY(A.Send(f[q] + (int64_t)P->nz * NN, pl, ncclDouble, P->rank + 1, comm, P->stream));
+        NCCL_TRY(A.Recv(f[q] + (int64_t)(P->nz + P->p) * NN, pl, ncclDouble, P->rank + 1, comm, P->stream));
+      }
+    }
+    NCCL_TRY(A.GroupEnd());
+    return ADI_OK;
+  }
+  adi_status z2y(adi_patch P, double* const* src, double* const* dst, int nf) override {
+    const NcclApi& A = nccl_api();
+    const int N = P->N, R = P->nrk;
+    const int64_t NN = (int64_t)N * N;
+    adi_status st;
+    // pack: block for rank s = own planes x rows [j0_s, j1_s), contiguous per destination
+    for (int q = 0; q < nf; q++) {
+      const double* in = src[q] + (int64_t)P->p * NN;
+      int64_t off = 0;
+      for (int t = 0; t < R; t++) {
+        const int64_t a = slab_lo(N, R, t), b = slab_lo(N, R, t + 1);
+        double* blk = P->xbuf[0] + (int64_t)q * P->UL + off;
+        if ((st = box_copy(P, blk, N, b - a, 0, 0, 0, in, N, N, 0, a, 0, N, b - a, P->nz))) return st;
+        off += (b - a) * N * P->nz;
+      }
+    }
+    NCCL_TRY(A.GroupStart());
+    for (int q = 0; q < nf; q++) {
+      int64_t off = 0;
+      for (int t = 0; t < R; t++) {
+        const int64_t a = slab_lo(N, R, t), b = slab_lo(N, R, t + 1);
+        const int64_t ka = slab_lo(N, R, t), kb = slab_lo(N, R, t + 1);
+        NCCL_TRY(A.Send(P->xbuf[0] + (int64_t)q * P->UL + off, (b - a) * N * P->nz, ncclDouble, t, comm, P->stream));
+        NCCL_TRY(A.Recv(dst[q] + ka * P->ny * N, (kb - ka) * P->ny * N, ncclDouble, t, comm, P->stream));
+        off += (b - a) * N * P->nz;
+      }
+    }
+    NCCL_TRY(A.GroupEnd());
+    return ADI_OK;
+  }
+  adi_status y2z(adi_patch P, double* const* src, double* const* dst, int nf) override {
+    const NcclApi& A = nccl_api();
+    const int N = P->N, R = P->nrk;
+    const int64_t NN = (int64_t)N * N;
+    NCCL_TRY(A.GroupStart());
+    for (int q = 0; q < nf; q++) {
+      int64_t off = 0;
+      for (int t = 0; t < R; t++) {
+        const int64_t ka = slab_lo(N, R, t), kb = slab_lo(N, R, t + 1);
+        const int64_t a = slab_lo(N, R, t), b = slab_lo(N, R, t + 1);
+        NCCL_TRY(A.Send(src[q] + ka * P->ny * N, (kb - ka) * P->ny * N, ncclDouble, t, comm, P->stream));
+        NCCL_TRY(A.Recv(P->xbuf[1] + (int64_t)q * P->UL + off, (b - a) * N * P->nz, ncclDouble, t, comm, P->stream));
+        off += (b - a) * N * P->nz;
+      }
+    }
+    NCCL_TRY(A.GroupEnd());
+    adi_status st;
+    for (int q = 0; q < nf; q++) {
+      double* out = dst[q] + (int64_t)P->p * NN;
+      int64_t off = 0;
+      for (int t = 0; t < R; t++) {
+        const int64_t a = slab_lo(N, R, t), b = slab_lo(N, R, t + 1);
+        const double* blk = P->xbuf[1] + (int64_t)q * P->UL + off;
+        if ((st = box_copy(P, out, N, N, 0, a, 0, blk, N, b - a, 0, 0, 0, N, b - a, P->nz))) return st;
+        off += (b - a) * N * P->nz;
+      }
+    }
+    return ADI_OK;
+  }
+};
+
+// ---- in-process loopback: R patches driven by R host threads on one device ----
+struct LoopGroup {
+  int R = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int count = 0;
+  long gen = 0;
+  bool aborted = false;
+  std::vector<adi_patch> patch;
+  std::vector<double* const*> post;
+  bool barrier() {  // false if a rank aborted
+    std::unique_lock<std::mutex> lk(m);
+    if (aborted) return false;
+    const long g = gen;
+    if (++count == R) {
+      count = 0;
+      gen++;
+      cv.notify_all();
+      return true;
+    }
+    // a rank that failed before reaching the exchange never arrives: give up after 10 minutes
+    if (!cv.wait_for(lk, std::chrono::minutes(10), [&] { return gen != g || aborted; })) aborted = true;
+    if (aborted) cv.notify_all();
+    return !aborted;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(m);
+    aborted = true;
+    cv.notify_all();
+  }
+};
+
+struct LoopTransport : Transport {
+  LoopGroup* g = nullptr;
+  bool capturable() const override { return false; }
+  // post this rank's pointers, wait for every rank (own stream drained first); op reads peers'
+  // buffers on the own stream; then drain and wait again so no peer overwrites before the reads
+  template <class F>
+  adi_status exchange(adi_patch P, double* const* mine, F&& op) {
+    cudaError_t e = cudaStreamSynchronize(P->stream);
+    if (e != cudaSuccess) {
+      g->abort();
+      return fail(ADI_ERR_CUDA, "loopback: %s", cudaGetErrorString(e));
+    }
+    g->post[P->rank] = mine;
+    if (!g->barrier()) return fail(ADI_ERR_NCCL, "loopback: a peer rank aborted");
+    adi_status st = op();
+    e = cudaStreamSynchronize(P->stream);
+    if (st == ADI_OK && e != cudaSuccess) st = fail(ADI_ERR_CUDA, "loopback: %s", cudaGetErrorString(e));
+    if (st != ADI_OK) {
+      g->abort();
+      return st;
+    }
+    if (!g->barrier()) return fail(ADI_ERR_NCCL, "loopback: a peer rank aborted");
+    return ADI_OK;
+  }
+  adi_status halo(adi_patch P, double* const* f, int nf) override {
+    return exchange(P, f, [&]() -> adi_status {
+      const int64_t NN = (int64_t)P->N * P->N, pl = (int64_t)P->p * NN;
+      for (int q = 0; q < nf; q++) {
+        if (P->rank > 0) {
+          adi_patch Q = g->patch[P->rank - 1];
+          CUDA_TRY(cudaMemcpyAsync(f[q], g->post[P->rank - 1][q] + (int64_t)Q->nz * NN, pl * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, P->stream));
+        }
+        if (P->rank < P->nrk - 1)
+          CUDA_TRY(cudaMemcpyAsync(f[q] + (int64_t)(P->nz + P->p) * NN, g->post[P->rank + 1][q] + pl,
+                                   pl * sizeof(double), cudaMemcpyDeviceToDevice, P->stream));
+      }
+      return ADI_OK;
+    });
+  }
+  adi_status z2y(adi_patch P, double* const* src, double* const* dst, int nf) override {
+    return exchange(P, src, [&]() -> adi_status {
+      const int N = P->N;
+      const int64_t NN = (int64_t)N * N;
+      adi_status st;
+      for (int q = 0; q < nf; q++)
+        for (int t = 0; t < P->nrk; t++) {
+          adi_patch Q = g->patch[t];
+          const double* in = g->post[t][q] + (int64_t)Q->p * NN;  // peer t's planes [k0_t, k1_t)
+          if ((st = box_copy(P, dst[q], N, P->ny, 0, 0, Q->k0, in, N, N, 0, P->j0, 0, N, P->ny, Q->nz))) return st;
+        }
+      return ADI_OK;
+    });
+  }
+  adi_status y2z(adi_patch P, double* const* src, double* const* dst, int nf) override {
+    return exchange(P, src, [&]() -> adi_status {
+      const int N = P->N;
+      const int64_t NN = (int64_t)N * N;
+      adi_status st;
+      for (int q = 0; q < nf; q++)
+        for (int t = 0; t < P->nrk; t++) {
+          adi_patch Q = g->patch[t];
+          const double* in = g->post[t][q];  // peer t's y-slab, rows [j0_t, j1_t), all planes
+          if ((st = box_copy(P, dst[q] + (int64_t)P->p * NN, N, N, 0, Q->j0, 0, in, N, Q->ny, 0, 0, P->k0, N, Q->ny,
+                             P->nz)))
+            return st;
+        }
+      return ADI_OK;
+    });
+  }
+};
+
+double* slab_inner(adi_patch P, double* f) { return f + (int64_t)P->p * P->N * P->N; }
+
+// One stage of sweeps in slab mode: x / y jobs on the z-slabs, z jobs on y-slabs between one
+// batched z -> y transpose of their inputs (DER: u and base) and one y -> z transpose back.
+// Jobs carry INNER z-slab pointers of halo'd buffers (in, out, base).
+adi_status dist_sweeps(adi_patch P, int mode, const SweepReq* jobs, int nj, const int* fam) {
+  SweepReq loc[3], zj[3];
+  int nl = 0, nzj = 0;
+  int zfam[3];
+  const int64_t NN = (int64_t)P->N * P->N;
+  for (int j = 0; j < nj; j++) {
+    SweepReq r = jobs[j];
+    if (r.axis != 2) {
+      r.dims[0] = P->N, r.dims[1] = P->N, r.dims[2] = P->nz;
+      r.c = P->c;
+      if (mode == adi::SW_MOD) r.iu = P->iu[fam[j]];
+      loc[nl++] = r;
+    } else {
+      zfam[nzj] = mode == adi::SW_MOD ? fam[j] : -1;
+      zj[nzj++] = r;
+    }
+  }
+  adi_status st;
+  if (nl && (st = launch_sweeps(P, loc, nl, mode))) return st;
+  if (!nzj) return ADI_OK;
+  // transpose in: inputs (and DER bases) -> Y
+  double* src[3];
+  double* dst[3];
+  const int per = mode == adi::SW_DER ? 2 : 1;
+  {
+    double* s_in[6];
+    double* d_in[6];
+    int nf = 0;
+    for (int q = 0; q < nzj; q++) {
+      s_in[nf] = const_cast<double*>(zj[q].in) - (int64_t)P->p * NN;  // halo'd buffer base
+      d_in[nf++] = P->Y[per * q];
+      if (per == 2) {
+        s_in[nf] = const_cast<double*>(zj[q].base) - (int64_t)P->p * NN;
+        d_in[nf++] = P->Y[per * q + 1];
+      }
+    }
+    for (int o = 0; o < nf; o += 3)
+      if ((st = P->tr->z2y(P, s_in + o, d_in + o, std::min(3, nf - o)))) return st;
+  }
+  SweepReq yj[3];
+  for (int q = 0; q < nzj; q++) {
+    SweepReq r = zj[q];
+    r.dims[0] = P->N, r.dims[1] = P->ny, r.dims[2] = P->N;
+    r.in = P->Y[per * q];
+    if (per == 2) {
+      r.base = P->Y[per * q + 1];
+      r.out = P->Y[per * q + 1];
+    } else {
+      r.out = P->Y[per * q];
+    }
+    r.c = P->cy;
+    if (mode == adi::SW_MOD) r.iu = P->iu[zfam[q]];
+    yj[q] = r;
+  }
+  if ((st = launch_sweeps(P, yj, nzj, mode))) return st;
+  for (int q = 0; q < nzj; q++) {
+    src[q] = yj[q].out;
+    dst[q] = zj[q].out - (int64_t)P->p * NN;
+  }
+  return P->tr->y2z(P, src, dst, nzj);
+}
+
+// One substep in slab mode (same operations and order as substep()).
+adi_status dist_substep(adi_patch P, int s) {
+  adi_status st;
+  const int p = P->p;
+  if ((st = P->tr->halo(P, P->F, 6))) return st;
+  // a1 / a5: RHS of the three E systems on the own planes (inputs with halos)
+  for (int d = 0; d < 3; d++) {
+    adi::RhsArgs args{};
+    args.u[0] = P->F[d];
+    args.u[1] = P->F[3 + (d + 2) % 3];
+    args.u[2] = P->F[3 + (d + 1) % 3];
+    args.u[3] = P->F[stiff_axis(s, d)];
+    args.nzin = P->nz + 2 * p;
+    args.zoff = p;
+    args.kg0 = P->k0;
+    args.nzout = P->nz;
+    args.load = P->load[d];
+    args.signal = P->signal;
+    args.nsig = P->nsig;
+    args.out = slab_inner(P, P->R[d]);
+    if ((st = launch_rhs(P, args, 0, s, d, ADI_K_RHS_E))) return st;
+  }
+  // a2 / a6: stiffened (row-modified) sweep first, then the mass sweeps in ascending axis order (D7)
+  {
+    SweepReq r[3];
+    int fam[3];
+    for (int d = 0; d < 3; d++) {
+      double* e = slab_inner(P, P->R[d]);
+      r[d] = SweepReq{d, stiff_axis(s, d), e, e, nullptr};
+      fam[d] = family(s, d);
+    }
+    if ((st = dist_sweeps(P, adi::SW_MOD, r, 3, fam))) return st;
+    for (int stage = 0; stage < 2; stage++) {
+      for (int d = 0; d < 3; d++) {
+        const int sg = stiff_axis(s, d);
+        int axes[2], k = 0;
+        for (int ax = 0; ax < 3; ax++)
+          if (ax != sg) axes[k++] = ax;
+        double* e = slab_inner(P, P->R[d]);
+        r[d] = SweepReq{d, axes[stage], e, e, nullptr};
+      }
+      if ((st = dist_sweeps(P, adi::SW_MASS, r, 3, fam))) return st;
+    }
+  }
+  if (P->mu_uniform && !P->h_general) {
+    // a3+a4 / a7+a8, uniform mu: the two derivative projections (see h_update_first / second)
+    const double b = P->b_scalar;
+    SweepReq r[3];
+    for (int d = 0; d < 3; d++) {
+      const int a1 = s == 1 ? (d + 1) % 3 : (d + 2) % 3, x1 = s == 1 ? (d + 2) % 3 : (d + 1) % 3;
+      r[d] = SweepReq{3 + d, a1, slab_inner(P, P->F[x1]), slab_inner(P, P->G[d]), nullptr, slab_inner(P, P->F[3 + d]),
+                      s == 1 ? -b : b};
+    }
+    if ((st = dist_sweeps(P, adi::SW_DER, r, 3, nullptr))) return st;
+    for (int d = 0; d < 3; d++) {
+      const int a2 = s == 1 ? (d + 2) % 3 : (d + 1) % 3, x2 = s == 1 ? (d + 1) % 3 : (d + 2) % 3;
+      r[d] = SweepReq{3 + d, a2, slab_inner(P, P->R[x2]), slab_inner(P, P->G[d]), nullptr, slab_inner(P, P->G[d]),
+                      s == 1 ? b : -b};
+    }
+    if ((st = dist_sweeps(P, adi::SW_DER, r, 3, nullptr))) return st;
+  } else {
+    // general mu: G from discrete2 / discrete4 (needs the halos of the new E), then M^-3
+    if ((st = P->tr->halo(P, P->R, 3))) return st;
+    for (int d = 0; d < 3; d++) {
+      adi::RhsArgs args{};
+      args.u[0] = P->F[3 + d];
+      if (s == 1) {
+        args.u[1] = P->F[(d + 2) % 3];
+        args.u[2] = P->R[(d + 1) % 3];
+      } else {
+        args.u[1] = P->F[(d + 1) % 3];
+        args.u[2] = P->R[(d + 2) % 3];
+      }
+      args.nzin = P->nz + 2 * p;
+      args.zoff = p;
+      args.kg0 = P->k0;
+      args.nzout = P->nz;
+      args.out = slab_inner(P, P->G[d]);
+      if ((st = launch_rhs(P, args, 1, s, 3 + d, ADI_K_RHS_H))) return st;
+    }
+    for (int ax = 0; ax < 3; ax++) {
+      SweepReq r[3];
+      for (int d = 0; d < 3; d++) {
+        double* g = slab_inner(P, P->G[d]);
+        r[d] = SweepReq{3 + d, ax, g, g, nullptr};
+      }
+      if ((st = dist_sweeps(P, adi::SW_MASS, r, 3, nullptr))) return st;
+    }
+  }
+  for (int d = 0; d < 3; d++) {
+    std::swap(P->F[d], P->R[d]);
+    std::swap(P->F[3 + d], P->G[d]);
   }
   return ADI_OK;
 }
@@ -814,8 +1392,12 @@ adi_status check_positive(adi_patch P, const double* d, int64_t n, const char* w
 // No-pivot banded LU of M + diag(c) S along `axis` for every fiber of
 // component comp: writes the pivots 1/u_kk to iu (N^3) and returns
 // ADI_ERR_SINGULAR on a pivot |u_kk| < 1e-14 max|row| (D12 gate).
-adi_status factor_into(adi_patch P, int comp, int axis, double* iu, unsigned long long* bad, int s_for_msg) {
+adi_status factor_into(adi_patch P, int comp, int axis, double* iu, unsigned long long* bad, int s_for_msg,
+                       const int64_t* dims = nullptr, const double* c = nullptr) {
   SweepReq r{comp, axis, nullptr, nullptr, nullptr};
+  if (dims)
+    for (int a = 0; a < 3; a++) r.dims[a] = dims[a];
+  r.c = c;
   adi::SweepBatch B = make_batch(P, &r, 1);
   unsigned long long init = ~0ull;
   CUDA_TRY(cudaMemcpyAsync(bad, &init, sizeof init, cudaMemcpyHostToDevice, P->stream));
@@ -832,13 +1414,25 @@ adi_status factor_into(adi_patch P, int comp, int axis, double* iu, unsigned lon
 }
 
 // Pivot caches of the six row-modified families (north star: factorisations
-// cached across steps), refreshed whenever c changes.
+// cached across steps), refreshed whenever c changes.  Slab mode: each family in the
+// layout its sweep runs in (z-stiffened families on the y-slab, the others on the z-slab).
 adi_status factorize(adi_patch P) {
   unsigned long long* bad;
   CUDA_TRY(cudaMallocAsync(&bad, sizeof(unsigned long long), P->stream));
   adi_status st = ADI_OK;
   for (int s = 1; s <= 2 && !st; s++)
-    for (int d = 0; d < 3 && !st; d++) st = factor_into(P, d, stiff_axis(s, d), P->iu[family(s, d)], bad, s);
+    for (int d = 0; d < 3 && !st; d++) {
+      const int ax = stiff_axis(s, d);
+      if (!P->slab) {
+        st = factor_into(P, d, ax, P->iu[family(s, d)], bad, s);
+      } else if (ax == 2) {
+        const int64_t dims[3] = {P->N, P->ny, P->N};
+        st = factor_into(P, d, ax, P->iu[family(s, d)], bad, s, dims, P->cy);
+      } else {
+        const int64_t dims[3] = {P->N, P->N, P->nz};
+        st = factor_into(P, d, ax, P->iu[family(s, d)], bad, s, dims, P->c);
+      }
+    }
   cudaFreeAsync(bad, P->stream);
   return st;
 }
@@ -847,7 +1441,20 @@ adi_status factorize(adi_patch P) {
 // a uniform mu^ (then b is the scalar of the derivative-projection H update).
 adi_status derive_abc(adi_patch P, double* epsh, double* muh) {
   drop_graph(P);  // kernel parameters (b, band constants) change with tau / materials
-  adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh, muh, P->tau, P->U, P->a, P->b, P->c);
+  if (!P->slab) {
+    adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh, muh, P->tau, P->U, P->a, P->b, P->c);
+  } else {
+    // z-slab rows: a contiguous slice of the global per-test-function arrays
+    const int64_t off = (int64_t)P->k0 * P->N * P->N;
+    adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh + off, muh + off, P->tau, P->UL, P->a, P->b, P->c);
+    CUDA_TRY(cudaGetLastError());
+    // y-slab: gather eps^, mu^ of rows [j0, j1) (Y buffers are scratch here), then c only
+    adi_status st;
+    const int N = P->N;
+    if ((st = box_copy(P, P->Y[0], N, P->ny, 0, 0, 0, epsh, N, N, 0, P->j0, 0, N, P->ny, N))) return st;
+    if ((st = box_copy(P, P->Y[1], N, P->ny, 0, 0, 0, muh, N, N, 0, P->j0, 0, N, P->ny, N))) return st;
+    adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(P->Y[0], P->Y[1], P->tau, P->UY, P->Y[2], P->Y[3], P->cy);
+  }
   CUDA_TRY(cudaGetLastError());
   unsigned long long* mm;
   CUDA_TRY(cudaMallocAsync(&mm, 2 * sizeof(unsigned long long), P->stream));
@@ -874,6 +1481,29 @@ extern "C" {
 
 const char* adi_last_error(void) { return g_err.c_str(); }
 
+adi_status adi_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(ADI_ERR_ARG, "adi_nccl_unique_id: id_out is NULL");
+  const NcclApi& A = nccl_api();
+  if (!A.ok) return fail(ADI_ERR_NCCL, "NCCL unavailable: %s", A.why.c_str());
+  ncclUniqueId id;
+  ncclResult_t r = A.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(ADI_ERR_NCCL, "ncclGetUniqueId: %s", A.GetErrorString(r));
+  memcpy(id_out, &id, sizeof id);
+  return ADI_OK;
+}
+
+adi_status adi_loopback_create(int32_t nranks, void** group_out) {
+  if (!group_out || nranks < 1) return fail(ADI_ERR_ARG, "adi_loopback_create: bad args");
+  auto* G = new LoopGroup();
+  G->R = nranks;
+  G->patch.assign(nranks, nullptr);
+  G->post.assign(nranks, nullptr);
+  *group_out = G;
+  return ADI_OK;
+}
+
+void adi_loopback_destroy(void* group) { delete static_cast<LoopGroup*>(group); }
+
 void adi_destroy(adi_patch P) {
   if (!P) return;
   cudaSetDevice(P->cfg.device);
@@ -889,6 +1519,15 @@ void adi_destroy(adi_patch P) {
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
   for (int i = 0; i < 6; i++) f(P->iu[i]);
+  for (int i = 0; i < 6; i++) f(P->Y[i]);
+  f(P->cy), f(P->xbuf[0]), f(P->xbuf[1]);
+  if (P->tr) {
+    if (auto* L = dynamic_cast<LoopTransport*>(P->tr)) {
+      std::lock_guard<std::mutex> lk(L->g->m);
+      if (L->g->patch[P->rank] == P) L->g->patch[P->rank] = nullptr;
+    }
+    delete P->tr;
+  }
   for (auto& e : P->ev_used) cudaEventDestroy(e.second.first), cudaEventDestroy(e.second.second);
   for (auto& e : P->ev_free) cudaEventDestroy(e);
   if (P->own_stream && P->stream) cudaStreamDestroy(P->stream);
@@ -907,6 +1546,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     return fail(ADI_ERR_ARG, "adi_create: rank %d of %d", cfg->rank, cfg->nranks);
   if (cfg->nranks > cfg->n + cfg->p)
     return fail(ADI_ERR_ARG, "adi_create: %d ranks for %d planes", cfg->nranks, cfg->n + cfg->p);
+  if (cfg->nccl_id && cfg->loopback) return fail(ADI_ERR_ARG, "adi_create: both nccl_id and loopback given");
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) return fail(ADI_ERR_CUDA, "cudaSetDevice(%d): %s", cfg->device, cudaGetErrorString(e));
   adi_patch P = new adi_patch_s();
@@ -936,6 +1576,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_H_GENERAL")) P->h_general = atoi(s);
   if (const char* s = getenv("ADI_SW_TWISTED")) P->use_tw = atoi(s);
   if (const char* s = getenv("ADI_OVERLAP")) P->overlap = atoi(s);
+  if (const char* s = getenv("ADI_SW_TMA")) P->use_st = atoi(s);
+  if (const char* s = getenv("ADI_SW_RES")) P->use_res = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   {
@@ -1062,9 +1704,59 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
       cudaMemcpy(P->d_sp[var], sp.data(), sp.size() * sizeof(double), cudaMemcpyHostToDevice);
     }
   }
-  // box mode (nranks > 1): the caller owns the slab buffers (adi_box_*); the patch
-  // keeps only the 1D operators, factor tables and sweep checkpoints.
+  // whole patch (nranks == 1): N^3 arrays.  Slab mode (nranks > 1 with a transport): the
+  // rank's z-slab (p halo planes per side) + y-slab work buffers, global eps^ / mu^.  Box mode
+  // (nranks > 1, no transport): the caller owns the slab buffers (adi_box_*); the patch keeps
+  // only the 1D operators, factor tables and sweep checkpoints.
   const bool whole = cfg->nranks == 1;
+  P->slab = cfg->nranks > 1 && (cfg->nccl_id || cfg->loopback);
+  P->nrk = cfg->nranks;
+  P->rank = cfg->rank;
+  if (P->slab) {
+    P->k0 = (int)slab_lo(N, P->nrk, P->rank), P->k1 = (int)slab_lo(N, P->nrk, P->rank + 1), P->nz = P->k1 - P->k0;
+    P->j0 = P->k0, P->j1 = P->k1, P->ny = P->nz;
+    P->UL = (int64_t)N * N * P->nz;
+    P->UH = (int64_t)N * N * (P->nz + 2 * p);
+    P->UY = (int64_t)N * P->ny * N;
+    for (int i = 0; i < 6; i++)
+      if (!dmalloc(&P->F[i], P->UH)) return bail(fail(ADI_ERR_OOM, "cudaMalloc slab fields"));
+    for (int i = 0; i < 3; i++)
+      if (!dmalloc(&P->R[i], P->UH) || !dmalloc(&P->G[i], P->UH)) return bail(fail(ADI_ERR_OOM, "cudaMalloc slab scratch"));
+    for (int i = 0; i < 6; i++)
+      if (!dmalloc(&P->Y[i], P->UY)) return bail(fail(ADI_ERR_OOM, "cudaMalloc y-slab buffers"));
+    if (!dmalloc(&P->a, P->UL) || !dmalloc(&P->b, P->UL) || !dmalloc(&P->c, P->UL) || !dmalloc(&P->cy, P->UY) ||
+        !dmalloc(&P->epsh, P->U) || !dmalloc(&P->muh, P->U))
+      return bail(fail(ADI_ERR_OOM, "cudaMalloc slab material arrays"));
+    for (int s = 1; s <= 2; s++)
+      for (int d = 0; d < 3; d++)
+        if (!dmalloc(&P->iu[family(s, d)], stiff_axis(s, d) == 2 ? P->UY : P->UL))
+          return bail(fail(ADI_ERR_OOM, "cudaMalloc slab pivot caches"));
+    for (int i = 0; i < 6; i++) cudaMemset(P->F[i], 0, P->UH * sizeof(double));
+    for (int i = 0; i < 3; i++) cudaMemset(P->R[i], 0, P->UH * sizeof(double)), cudaMemset(P->G[i], 0, P->UH * sizeof(double));
+    if (cfg->nccl_id) {
+      const NcclApi& A = nccl_api();
+      if (!A.ok) return bail(fail(ADI_ERR_NCCL, "NCCL unavailable: %s", A.why.c_str()));
+      if (!dmalloc(&P->xbuf[0], 3 * P->UL) || !dmalloc(&P->xbuf[1], 3 * P->UL))
+        return bail(fail(ADI_ERR_OOM, "cudaMalloc transpose buffers"));
+      auto* T = new NcclTransport();
+      P->tr = T;
+      ncclUniqueId id;
+      memcpy(&id, cfg->nccl_id, sizeof id);
+      ncclResult_t r = A.CommInitRank(&T->comm, P->nrk, id, P->rank);
+      if (r != ncclSuccess) {
+        T->comm = nullptr;
+        return bail(fail(ADI_ERR_NCCL, "ncclCommInitRank: %s", A.GetErrorString(r)));
+      }
+    } else {
+      auto* G = static_cast<LoopGroup*>(cfg->loopback);
+      if (G->R != P->nrk) return bail(fail(ADI_ERR_ARG, "adi_create: loopback group of %d ranks, nranks %d", G->R, P->nrk));
+      auto* T = new LoopTransport();
+      T->g = G;
+      P->tr = T;
+      std::lock_guard<std::mutex> lk(G->m);
+      G->patch[P->rank] = P;
+    }
+  }
   const size_t U = whole ? (size_t)P->U : 0;
   for (int i = 0; i < 6 && whole; i++)
     if (!dmalloc(&P->F[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc fields (%zu doubles)", U));
@@ -1088,6 +1780,9 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
       words = std::max<int64_t>(words, (int64_t)std::max(P->sw_grid[m], P->sw_grid_tw[m]) * adi::SW_WARPS *
                                            ((N + adi::sw_ch(m) - 1) / adi::sw_ch(m)) *
                                            std::max(adi::sw_state_words(m, p), adi::sw_state_words_tw(m, p)) * 32);
+    for (int m = 0; m < 3; m++)  // TMA-staged sweeps: 16-row chunks, P^2 (MOD) or P state words
+      words = std::max<int64_t>(words, (int64_t)P->st_grid[m] * adi::st_warps(m) * ((N + adi::ST_CH - 1) / adi::ST_CH) *
+                                           adi::st_state_words(m, p) * 32);
     P->ckpt_words = (size_t)words;
     if (!dmalloc(&P->ckpt, P->ckpt_words) || !dmalloc(&P->ckpt2, P->ckpt_words))
       return bail(fail(ADI_ERR_OOM, "cudaMalloc sweep checkpoints"));
@@ -1098,8 +1793,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   }
   if (cudaMalloc(&P->d_step, sizeof(int64_t)) != cudaSuccess) return bail(fail(ADI_ERR_OOM, "cudaMalloc step"));
   cudaMemset(P->d_step, 0, sizeof(int64_t));
-  if (whole) {
-    for (int i = 0; i < 6; i++) cudaMemset(P->F[i], 0, U * sizeof(double));
+  if (whole || P->slab) {
+    for (int i = 0; i < 6 && whole; i++) cudaMemset(P->F[i], 0, U * sizeof(double));
     // eps = mu = 1
     adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->epsh, P->U, 1.0);
     adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->muh, P->U, 1.0);
@@ -1135,7 +1830,8 @@ adi_status adi_layout(adi_patch P, int64_t* N, int64_t* k0, int64_t* k1) {
 
 adi_status adi_set_tau(adi_patch P, double tau) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (!(tau > 0.0) || !std::isfinite(tau)) return fail(ADI_ERR_ARG, "adi_set_tau: tau must be finite and > 0");
   const double old = P->tau;
   P->tau = tau;
@@ -1171,7 +1867,8 @@ static adi_status set_tf(adi_patch P, double* eps_new, double* mu_new) {
 
 adi_status adi_set_materials_tf(adi_patch P, const double* eps_tf, const double* mu_tf) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (!eps_tf) return fail(ADI_ERR_ARG, "adi_set_materials_tf: eps is NULL");
   double *e = nullptr, *m = nullptr;
   if (cudaMalloc(&e, P->U * sizeof(double)) != cudaSuccess || cudaMalloc(&m, P->U * sizeof(double)) != cudaSuccess) {
@@ -1214,7 +1911,8 @@ static adi_status map_elements(adi_patch P, const double* d_elem, double* d_out,
 
 adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* mu_elem) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (!eps_elem) return fail(ADI_ERR_ARG, "adi_set_materials: eps is NULL");
   const int64_t ne = (int64_t)P->n * P->n * P->n;
   double *de = nullptr, *dw = nullptr, *e = nullptr, *m = nullptr;
@@ -1251,17 +1949,23 @@ adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* 
 
 adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (!f) return fail(ADI_ERR_ARG, "adi_set_fields: NULL array");
   for (int c = 0; c < 6; c++)
     if (!f[c]) return fail(ADI_ERR_ARG, "adi_set_fields: field %d is NULL", c);
   for (int c = 0; c < 6; c++) {
-    adi_status st = copy_in(P, P->F[c], f[c], P->U);
+    double* dst = P->slab ? slab_inner(P, P->F[c]) : P->F[c];
+    adi_status st = copy_in(P, dst, f[c], P->slab ? P->UL : P->U);
     if (st) return poison(P, st);
     if (c < 3 && P->cfg.bc == ADI_BC_PEC) {
       int lo[3], hi[3];
       for (int ax = 0; ax < 3; ax++) active_range(P, c, ax, lo[ax], hi[ax]);
-      adi::pec_zero_kernel<<<148 * 8, 256, 0, P->stream>>>(P->F[c], P->N, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]);
+      if (P->slab)
+        adi::pec_box_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(dst, P->N, P->N, P->nz, 0, 0, P->k0, lo[0], hi[0], lo[1],
+                                                               hi[1], lo[2], hi[2]);
+      else
+        adi::pec_zero_kernel<<<148 * 8, 256, 0, P->stream>>>(P->F[c], P->N, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]);
     }
   }
   cudaError_t e = cudaStreamSynchronize(P->stream);
@@ -1272,11 +1976,13 @@ adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
 
 adi_status adi_get_fields(adi_patch P, double* const f[6]) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (!f) return fail(ADI_ERR_ARG, "adi_get_fields: NULL array");
   for (int c = 0; c < 6; c++) {
     if (!f[c]) continue;
-    cudaError_t e = cudaMemcpyAsync(f[c], P->F[c], P->U * sizeof(double), cudaMemcpyDefault, P->stream);
+    const double* src = P->slab ? slab_inner(P, P->F[c]) : P->F[c];
+    cudaError_t e = cudaMemcpyAsync(f[c], src, (P->slab ? P->UL : P->U) * sizeof(double), cudaMemcpyDefault, P->stream);
     if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_get_fields: %s", cudaGetErrorString(e)));
   }
   cudaError_t e = cudaStreamSynchronize(P->stream);
@@ -1286,7 +1992,8 @@ adi_status adi_get_fields(adi_patch P, double* const f[6]) {
 
 adi_status adi_set_source(adi_patch P, const double* const load[3], const double* signal, int64_t nsig) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (nsig < 0) return fail(ADI_ERR_ARG, "adi_set_source: nsig < 0");
   drop_graph(P);
   cudaStreamSynchronize(P->stream);
@@ -1300,11 +2007,13 @@ adi_status adi_set_source(adi_patch P, const double* const load[3], const double
   if (!load || !signal || nsig == 0) return ADI_OK;
   for (int d = 0; d < 3; d++) {
     if (!load[d]) continue;
-    if (cudaMalloc(&P->load[d], P->U * sizeof(double)) != cudaSuccess) {
+    // slab mode: the global load vector's z-slab rows (a contiguous slice)
+    const int64_t cnt = P->slab ? P->UL : P->U, off = P->slab ? (int64_t)P->k0 * P->N * P->N : 0;
+    if (cudaMalloc(&P->load[d], cnt * sizeof(double)) != cudaSuccess) {
       cudaGetLastError();
       return fail(ADI_ERR_OOM, "adi_set_source: cudaMalloc");
     }
-    adi_status st = copy_in(P, P->load[d], load[d], P->U);
+    adi_status st = copy_in(P, P->load[d], load[d] + off, cnt);
     if (st) return poison(P, st);
   }
   if (cudaMalloc(&P->signal, nsig * sizeof(double)) != cudaSuccess) {
@@ -1353,12 +2062,13 @@ static adi_status run_steps(adi_patch P, int64_t k) {
 
 adi_status adi_step(adi_patch P, int64_t k) {
   CHECK_PATCH(P);
-  if (P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1): use the adi_box_* entry points");
+  if (P->cfg.nranks != 1 && !P->slab)
+    return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (k < 0) return fail(ADI_ERR_ARG, "adi_step: k < 0");
   if (!P->have_fields) return fail(ADI_ERR_STATE, "adi_step: fields not set");
   if (k == 0) return ADI_OK;
   adi_status st = ADI_OK;
-  if (P->timing) {
+  if (P->timing || (P->slab && !P->tr->capturable())) {
     st = run_steps(P, k);
   } else {
     if (!P->graph) {
@@ -1558,17 +2268,8 @@ adi_status adi_box_sweep(adi_patch P, int32_t mode, int32_t njobs, const adi_swe
     r[j] = SweepReq{J.comp, J.axis, J.in, J.out, J.iu, J.base, J.coef, {J.dims[0], J.dims[1], J.dims[2]}};
   }
   // the modified sweeps read c from the job (box layout), not from the patch
-  const bool tw = twisted(P, r, njobs, mode);
-  adi::SweepBatch B = make_batch(P, r, njobs, tw ? 16 : 32);
-  for (int j = 0; j < njobs; j++) B.job[j].c = jobs[j].c;
-  B.nck = (P->N + adi::sw_ch(mode) - 1) / adi::sw_ch(mode);
-  LaunchScope ls(P, mode == adi::SW_MOD ? ADI_K_SWEEP_MOD : mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS);
-  const int64_t blocks_needed = ((int64_t)B.ntiles + adi::SW_WARPS - 1) / adi::SW_WARPS;
-  const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, tw ? P->sw_grid_tw[mode] : P->sw_grid[mode]);
-  with_degree(P->p, [&](auto ops) { ops.sweep(P->stream, grid, B, mode, tw); });
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_box_sweep: %s", cudaGetErrorString(e)));
-  return ADI_OK;
+  for (int j = 0; j < njobs; j++) r[j].c = jobs[j].c;
+  return poison(P, launch_sweeps(P, r, njobs, mode));
 }
 
 adi_status adi_box_factor(adi_patch P, int32_t comp, int32_t axis, const int64_t dims[3], const double* c, double* iu) {

@@ -8,6 +8,29 @@
 
 namespace adi {
 
+#ifdef ADI_STUB
+// Tuning builds (tools/build_variant.py --degrees): this degree is not compiled; every entry
+// point reports cudaErrorNotSupported (adi_create then fails for this p).
+template <>
+void Ops<ADI_P>::rhs(cudaStream_t, dim3, const RhsArgs&, const RhsMaps&, bool, int, int, int) {}
+template <>
+cudaError_t Ops<ADI_P>::rhs_attrs() { return cudaErrorNotSupported; }
+template <>
+void Ops<ADI_P>::sweep(cudaStream_t, unsigned, const SweepBatch&, int, bool) {}
+template <>
+cudaError_t Ops<ADI_P>::sweep_attrs(int*, int*) { return cudaErrorNotSupported; }
+template <>
+void Ops<ADI_P>::sweep_tma(cudaStream_t, unsigned, const SweepBatch&, const SweepTmaMaps&, int) {}
+template <>
+cudaError_t Ops<ADI_P>::sweep_tma_attrs(int*) { return cudaErrorNotSupported; }
+template <>
+void Ops<ADI_P>::factor(cudaStream_t, unsigned, const SweepBatch&, double*, unsigned long long*, double) {}
+template <>
+void Ops<ADI_P>::sweep_res(cudaStream_t, unsigned, unsigned, size_t, const SweepBatch&, const SweepResMaps&, int) {}
+template <>
+cudaError_t Ops<ADI_P>::sweep_res_attrs() { return cudaErrorNotSupported; }
+#else
+
 namespace {
 template <int KIND, int S, int D>
 struct RhsF {
@@ -88,9 +111,54 @@ cudaError_t Ops<ADI_P>::sweep_attrs(int occ[3], int occ_tw[3]) {
 }
 
 template <>
+void Ops<ADI_P>::sweep_tma(cudaStream_t st, unsigned grid, const SweepBatch& B, const SweepTmaMaps& maps, int mode) {
+  if (mode == SW_MOD)
+    sweep_tma_kernel<ADI_P, SW_MOD><<<grid, 32 * st_warps(SW_MOD), st_smem_bytes<SW_MOD>(), st>>>(B, maps);
+  else if (mode == SW_DER)
+    sweep_tma_kernel<ADI_P, SW_DER><<<grid, 32 * st_warps(SW_DER), st_smem_bytes<SW_DER>(), st>>>(B, maps);
+  else
+    sweep_tma_kernel<ADI_P, SW_MASS><<<grid, 32 * st_warps(SW_MASS), st_smem_bytes<SW_MASS>(), st>>>(B, maps);
+}
+
+namespace {
+template <int MODE>
+cudaError_t st_attr(int* occ) {
+  auto k = sweep_tma_kernel<ADI_P, MODE>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st_smem_bytes<MODE>());
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, 32 * st_warps(MODE), st_smem_bytes<MODE>());
+}
+}  // namespace
+
+template <>
+cudaError_t Ops<ADI_P>::sweep_tma_attrs(int occ[3]) {
+  cudaError_t e;
+  if ((e = st_attr<SW_MASS>(&occ[SW_MASS]))) return e;
+  if ((e = st_attr<SW_MOD>(&occ[SW_MOD]))) return e;
+  return st_attr<SW_DER>(&occ[SW_DER]);
+}
+
+template <>
+void Ops<ADI_P>::sweep_res(cudaStream_t st, unsigned grid, unsigned warps, size_t smem, const SweepBatch& B,
+                           const SweepResMaps& maps, int mode) {
+  if (mode == SW_DER) sweep_res_kernel<ADI_P, SW_DER><<<grid, 32 * warps, smem, st>>>(B, maps);
+  else sweep_res_kernel<ADI_P, SW_MASS><<<grid, 32 * warps, smem, st>>>(B, maps);
+}
+
+template <>
+cudaError_t Ops<ADI_P>::sweep_res_attrs() {
+  const int mx = 227 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(sweep_res_kernel<ADI_P, SW_MASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(sweep_res_kernel<ADI_P, SW_DER>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
+template <>
 void Ops<ADI_P>::factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad,
                         double tol) {
   factor_kernel<ADI_P><<<grid, 128, 0, st>>>(B, iu, bad, tol);
 }
+
+#endif  // ADI_STUB
 
 }  // namespace adi

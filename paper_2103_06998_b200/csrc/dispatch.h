@@ -10,6 +10,8 @@
 #include "rhs.cuh"
 #include "sweep.cuh"
 #include "sweep_tw.cuh"
+#include "sweep_tma.cuh"
+#include "sweep_res.cuh"
 
 namespace adi {
 
@@ -27,6 +29,16 @@ struct Ops {
   // Set the dynamic shared memory of the sweep kernels; occ[mode] / occ_tw[mode] =
   // resident blocks per SM (SweepMode order: mass, modified, derivative projection).
   static cudaError_t sweep_attrs(int occ[3], int occ_tw[3]);
+  // One batched sweep launch of the TMA-staged kernel (sweep_tma.cuh); grid = blocks of
+  // st_warps(mode) warps, one block per SM.
+  static void sweep_tma(cudaStream_t st, unsigned grid, const SweepBatch& B, const SweepTmaMaps& maps, int mode);
+  // dynamic shared memory of the TMA-staged sweeps; occ[mode] = resident blocks per SM
+  static cudaError_t sweep_tma_attrs(int occ[3]);
+  // Fiber-resident two-segment sweep (sweep_res.cuh; modes SW_MASS / SW_DER): one block of
+  // `warps` warps per SM, `smem` dynamic shared bytes.
+  static void sweep_res(cudaStream_t st, unsigned grid, unsigned warps, size_t smem, const SweepBatch& B,
+                        const SweepResMaps& maps, int mode);
+  static cudaError_t sweep_res_attrs();
   // Pivot cache of one row-modified family (job 0 of B).
   static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };

@@ -1,5 +1,13 @@
 """Slab-decomposed ADI step across GPUs.
 
+The product path is the library's own distributed schedule (``adi_step`` on a patch created
+with ``nranks > 1`` and an NCCL unique id, include/adi_maxwell.h): ``create_patch`` below only
+broadcasts the id over ``torch.distributed`` and creates this rank's patch.
+
+``DistPatch`` is the same schedule written out in Python over the library's box-level calls
+(``adi_box_*``); it drives the gloo CPU tests (tests/test_dist_cpu.py, with a CPU test double
+of the box kernels) and documents the orchestration step by step:
+
 One process per GPU.  Rank r of R owns the z-planes [r N / R, (r+1) N / R) of the
 global N^3 coefficient grid (``adi_layout``).  Per substep:
 
@@ -28,6 +36,20 @@ try:
     import torch.distributed as tdist
 except Exception:  # pragma: no cover
     tdist = None
+
+
+def create_patch(n: int, p: int, tau: float, bc: int = 0, device: int | None = None, group=None):
+    """This rank's patch of a distributed run: rank 0 creates the NCCL unique id
+    (adi_nccl_unique_id), every rank receives it over torch.distributed and creates its z-slab
+    patch; the library then owns the NCCL communicator and runs every exchange itself."""
+    import paper_2103_06998_b200 as adi
+
+    rank, R = tdist.get_rank(group), tdist.get_world_size(group)
+    obj = [adi.nccl_unique_id() if rank == 0 else None]
+    tdist.broadcast_object_list(obj, src=0, group=group)
+    if device is None:
+        device = torch.cuda.current_device()
+    return adi.Patch(n, p, tau, bc, device=device, rank=rank, nranks=R, nccl_id=obj[0])
 
 
 def split(N: int, R: int, r: int):

@@ -529,3 +529,69 @@ def test_set_tau_singular_keeps_state():
     G.step(2)
     O.step(2)
     assert max(rel(a, b) for a, b in zip(G.get_fields(), O.get_fields())) <= TOL_STEP
+
+
+class _env:
+    """Set environment variables (the library reads its kernel-selection knobs at adi_create)."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        import os
+        self.old = {k: os.environ.get(k) for k in self.kv}
+        os.environ.update(self.kv)
+
+    def __exit__(self, *a):
+        import os
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,p", [(8, 2), (34, 2), (47, 3), (65, 1), (60, 4), (128, 2)])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+@pytest.mark.parametrize("knobs", [dict(ADI_SW_TMA="7"), dict(ADI_SW_RES="1")])
+def test_sweeps_tma_staged(n, p, axis, knobs):
+    """The TMA-staged sweep kernel (sweep_tma.cuh: even N, 16-row chunks, 32-fiber boxes with a
+    ragged last box per row, swizzled x boxes; ADI_SW_TMA=7 puts the row-modified mode on it too)
+    and the fiber-resident two-segment kernel (sweep_res.cuh, ADI_SW_RES=1: mass sweeps) against
+    the oracle for every PEC variant; N = 10 .. 130, one to nine chunks."""
+    with _env(**knobs):
+        O, G = both(n, p, 0.05)
+    N = n + p
+    assert N % 2 == 0
+    eps = workloads.random_tf(N, 13 + axis, 1.0, 80.0)
+    O.set_materials_tf(eps)
+    G.set_materials_tf(eps)
+    rng = np.random.default_rng(100 + axis)
+    for comp in (0, 1, 2, 4):
+        rhs = rng.uniform(-1, 1, N ** 3)
+        if comp < 3:
+            u = rhs.reshape(N, N, N)
+            for ax in range(3):
+                if ax != comp:
+                    sl = [slice(None)] * 3
+                    sl[2 - ax] = [0, N - 1]
+                    u[tuple(sl)] = 0.0
+        for mod in (False, True):
+            if comp > 2 and mod:
+                continue
+            ref = O.sweep(comp, axis, mod, rhs)
+            got = G.sweep(comp, axis, mod, rhs)
+            assert rel(got, ref) <= 1e-12, (comp, mod, rel(got, ref))
+
+
+@pytest.mark.parametrize("knobs", [dict(ADI_SW_TMA="0"), dict(ADI_SW_TMA="7"), dict(ADI_SW_RES="1")],
+                         ids=["legacy", "tma-all", "resident"])
+def test_tma_and_legacy_sweeps_full_steps(knobs):
+    """Full steps with every sweep-kernel selection -- the legacy cp.async kernel (ADI_SW_TMA=0),
+    the TMA-staged kernel for all three modes (ADI_SW_TMA=7), the fiber-resident two-segment
+    kernel for the mass / derivative modes (ADI_SW_RES=1) -- match the oracle: N = 36 (p = 2)
+    and N = 32 (p = 3), phantom."""
+    with _env(**knobs):
+        for n, p in [(34, 2), (29, 3)]:
+            errs, _ = _parity_run(n, p, 0.01, 3, material="phantom4")
+            assert max(errs) <= TOL_STEP, (n, p, errs)
