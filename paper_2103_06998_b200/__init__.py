@@ -22,7 +22,7 @@ _ROOT = os.path.dirname(_HERE)
 # ADI_LIB selects another build of the library (tuning experiments); default: the in-tree build
 LIB_PATH = os.environ.get("ADI_LIB") or os.path.join(_HERE, "lib", "libadimaxwell.so")
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh", "sweep_tw.cuh", "sweep_tma.cuh", "sweep_res.cuh")] + [
+SOURCES = [os.path.join(CSRC, f) for f in ("adi_maxwell.cu", "degree.cu", "rhs.cuh", "dispatch.h", "setup_kernels.cuh", "sweep.cuh", "sweep_tw.cuh", "sweep_tma.cuh", "sweep_res.cuh", "rhs3.cuh")] + [
     os.path.join(_ROOT, "include", "adi_maxwell.h")]
 DEGREES = (1, 2, 3, 4, 5)
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -220,6 +220,8 @@ struct adi_patch_s {
   // cp.async kernel, whose pass-2 working set (f, c, pivots) fits L2 better at its warp count.
   int use_st = (1 << 0) | (1 << 2);
   int st_grid[3] = {0, 0, 0};  // blocks of the TMA-staged sweep per mode (one per SM)
+  int use_rhs3 = 1;  // fused three-component RHS_E (rhs3.cuh) where possible; ADI_RHS3=0 disables
+  bool rhs3_ok = false;
   int use_res = 0;   // fiber-resident two-segment sweeps (sweep_res.cuh), opt-in (ADI_SW_RES=1): measured slower at c5
   bool res_ok = false;
   // ---- distributed (slab) mode: nranks > 1 with a transport ----
@@ -415,6 +417,50 @@ adi_status rhs_e(adi_patch P, int s, int d, const double* const E[3], const doub
   args.nsig = P->nsig;
   args.out = out;
   return launch_rhs(P, args, 0, s, d, ADI_K_RHS_E);
+}
+
+// The three E right-hand sides of substep s in one launch (rhs3.cuh): fields F[0..5] (E1..H3),
+// outputs out[0..2].  Whole patch: zin = 0; slab mode: halo'd inputs of nzin planes, the
+// rank's planes [kg0, kg0 + nzout) at input offset zoff.  false: not applicable (degree > 3,
+// odd N, no TMA map) -- the caller falls back to rhs_e per component.
+bool rhs_e3(adi_patch P, int s, double* const F[6], double* const out[3], int nzin, int zoff, int kg0, int nzout,
+            adi_status& st) {
+  if (!P->rhs3_ok || !P->use_tma) return false;
+  const int N = P->N, p = P->p;
+  adi::Rhs3Maps maps;
+  memset(&maps, 0, sizeof maps);
+  if (nzin == 0) nzin = nzout = N, zoff = kg0 = 0;
+  for (int f = 0; f < 6; f++)
+    if (!make_field_map(&maps.m[f], F[f], N, nzin, p)) return false;
+  adi::Rhs3Args args{};
+  args.N = N;
+  args.nzin = nzin, args.zoff = zoff, args.kg0 = kg0, args.nzout = nzout;
+  args.kchunk = rhs_kchunk(P, nzout);
+  args.tab = P->d_tab;
+  args.a = P->a;
+  args.c = P->c;
+  for (int d = 0; d < 3; d++) {
+    args.load[d] = P->load[d];
+    args.out[d] = out[d];
+    for (int ax = 0; ax < 3; ax++) active_range(P, d, ax, args.lo[d][ax], args.hi[d][ax]);
+  }
+  args.signal = P->signal;
+  args.nsig = P->nsig;
+  args.step = P->d_step;
+  {
+    const int W = P->W, r = N / 2;
+    for (int o = 0; o < 3; o++)
+      for (int q = 0; q < 11; q++) args.kint[o][q] = q < W ? P->tab_host[((size_t)o * N + r) * W + q] : 0.0;
+  }
+  const int ntx = (N + adi::RX_TX - 1) / adi::RX_TX, nty = (N + adi::RX_TY - 1) / adi::RX_TY;
+  const int fx = std::max(0, (N - 2 * p) / adi::RX_TX - 1), fy = std::max(0, (N - 2 * p) / adi::RX_TY - 1);
+  args.ntx = ntx, args.nty = nty, args.fx = fx && fy ? fx : 0, args.fy = fx && fy ? fy : 0;
+  const int nch = (nzout + args.kchunk - 1) / args.kchunk;
+  LaunchScope ls(P, ADI_K_RHS_E);
+  with_degree(p, [&](auto ops) { ops.rhs3(P->stream, dim3(ntx * nty, 1, nch), args, maps, s); });
+  cudaError_t e = cudaGetLastError();
+  st = e == cudaSuccess ? ADI_OK : fail(ADI_ERR_CUDA, "rhs3 launch: %s", cudaGetErrorString(e));
+  return true;
 }
 
 // RHS of the H system of component d, substep s (a3/a7); inputs of adi::RhsProg<1,s,d>.
@@ -774,8 +820,15 @@ adi_status substep(adi_patch P, int s) {
     if ((st = h_update_first(P, s, H, E, P->G, P->stream2, P->ckpt2))) return st;
     CUDA_TRY(cudaEventRecord(P->ev_join, P->stream2));
   }
-  for (int d = 0; d < 3; d++)
-    if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
+  {
+    adi_status st3 = ADI_OK;
+    if (rhs_e3(P, s, P->F, P->R, 0, 0, 0, 0, st3)) {
+      if (st3) return st3;
+    } else {
+      for (int d = 0; d < 3; d++)
+        if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
+    }
+  }
   if ((st = solve_e_range(P, s, 0, 3, P->R, P->R))) return st;
   const double* En[3] = {P->R[0], P->R[1], P->R[2]};
   if (fork) {
@@ -1137,7 +1190,11 @@ adi_status dist_substep(adi_patch P, int s) {
   const int p = P->p;
   if ((st = P->tr->halo(P, P->F, 6))) return st;
   // a1 / a5: RHS of the three E systems on the own planes (inputs with halos)
-  for (int d = 0; d < 3; d++) {
+  double* Rin[3] = {slab_inner(P, P->R[0]), slab_inner(P, P->R[1]), slab_inner(P, P->R[2])};
+  adi_status st3 = ADI_OK;
+  const bool fused = rhs_e3(P, s, P->F, Rin, P->nz + 2 * p, p, P->k0, P->nz, st3);
+  if (fused && st3) return st3;
+  for (int d = 0; d < 3 && !fused; d++) {
     adi::RhsArgs args{};
     args.u[0] = P->F[d];
     args.u[1] = P->F[3 + (d + 2) % 3];
@@ -1578,12 +1635,18 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_OVERLAP")) P->overlap = atoi(s);
   if (const char* s = getenv("ADI_SW_TMA")) P->use_st = atoi(s);
   if (const char* s = getenv("ADI_SW_RES")) P->use_res = atoi(s);
+  if (const char* s = getenv("ADI_RHS3")) P->use_rhs3 = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
+  if (P->use_rhs3 && p <= 3) {
+    P->rhs3_ok = with_degree(p, [](auto ops) { return ops.rhs3_attrs(); }) == cudaSuccess;
+    if (!P->rhs3_ok) cudaGetLastError();
+  }
   {
     const char* s = getenv("ADI_RHS_CPA");
     // TMA boxes no larger than the tensor (small patches use the cp.async kernel)
-    P->use_tma = (N % 2 == 0) && N >= adi::RX_TX + 2 * p && tma_encoder() != nullptr && !(s && atoi(s));
+    // (p >= 2: the p = 1 halo box {34, 18} faulted in the fused RHS kernel; p = 1 takes cp.async)
+    P->use_tma = p >= 2 && (N % 2 == 0) && N >= adi::RX_TX + 2 * p && tma_encoder() != nullptr && !(s && atoi(s));
   }
   Space1D sp(P->n, p);
   assemble_1d(sp, P->M, P->S, P->A);
@@ -2220,7 +2283,10 @@ adi_status adi_debug_rhs_e(adi_patch P, int32_t s, double* const R[3]) {
   if (st) return st;
   const double* E[3] = {P->F[0], P->F[1], P->F[2]};
   const double* H[3] = {P->F[3], P->F[4], P->F[5]};
-  for (int d = 0; d < 3 && !st; d++) st = rhs_e(P, s, d, E, H, t[d]);
+  adi_status st3 = ADI_OK;
+  if (rhs_e3(P, s, P->F, t, 0, 0, 0, 0, st3)) st = st3;  // the fused kernel where the step uses it
+  else
+    for (int d = 0; d < 3 && !st; d++) st = rhs_e(P, s, d, E, H, t[d]);
   for (int d = 0; d < 3 && !st; d++)
     if (R[d] && cudaMemcpyAsync(R[d], t[d], P->U * sizeof(double), cudaMemcpyDefault, P->stream) != cudaSuccess)
       st = fail(ADI_ERR_CUDA, "copy out");

@@ -16,6 +16,10 @@ void Ops<ADI_P>::rhs(cudaStream_t, dim3, const RhsArgs&, const RhsMaps&, bool, i
 template <>
 cudaError_t Ops<ADI_P>::rhs_attrs() { return cudaErrorNotSupported; }
 template <>
+void Ops<ADI_P>::rhs3(cudaStream_t, dim3, const Rhs3Args&, const Rhs3Maps&, int) {}
+template <>
+cudaError_t Ops<ADI_P>::rhs3_attrs() { return cudaErrorNotSupported; }
+template <>
 void Ops<ADI_P>::sweep(cudaStream_t, unsigned, const SweepBatch&, int, bool) {}
 template <>
 cudaError_t Ops<ADI_P>::sweep_attrs(int*, int*) { return cudaErrorNotSupported; }
@@ -78,6 +82,28 @@ cudaError_t Ops<ADI_P>::rhs_attrs() {
   acc(rhs_attr_one<1, 1, 0>()); acc(rhs_attr_one<1, 1, 1>()); acc(rhs_attr_one<1, 1, 2>());
   acc(rhs_attr_one<1, 2, 0>()); acc(rhs_attr_one<1, 2, 1>()); acc(rhs_attr_one<1, 2, 2>());
   return e;
+}
+
+template <>
+void Ops<ADI_P>::rhs3(cudaStream_t st, dim3 grid, const Rhs3Args& args, const Rhs3Maps& maps, int s) {
+#if ADI_P <= 3
+  constexpr size_t smem = rhs3_smem_bytes<ADI_P>();
+  if (s == 1) rhs3_kernel<ADI_P, 1><<<grid, RX_THREADS, smem, st>>>(maps, args);
+  else rhs3_kernel<ADI_P, 2><<<grid, RX_THREADS, smem, st>>>(maps, args);
+#endif
+}
+
+template <>
+cudaError_t Ops<ADI_P>::rhs3_attrs() {
+#if ADI_P <= 3
+  constexpr size_t smem = rhs3_smem_bytes<ADI_P>();
+  const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaFuncSetAttribute(rhs3_kernel<ADI_P, 1>, A, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(rhs3_kernel<ADI_P, 2>, A, (int)smem);
+#else
+  return cudaErrorNotSupported;  // degrees 4, 5: the per-component rhs_kernel
+#endif
 }
 
 template <>

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include "rhs.cuh"
+#include "rhs3.cuh"
 #include "sweep.cuh"
 #include "sweep_tw.cuh"
 #include "sweep_tma.cuh"
@@ -23,6 +24,9 @@ struct Ops {
   static void rhs(cudaStream_t st, dim3 grid, const RhsArgs& args, const RhsMaps& maps, bool tma, int kind,
                   int s, int d);
   static cudaError_t rhs_attrs();
+  // The three E right-hand sides of substep s in one launch (rhs3.cuh; TMA, P <= 3).
+  static void rhs3(cudaStream_t st, dim3 grid, const Rhs3Args& args, const Rhs3Maps& maps, int s);
+  static cudaError_t rhs3_attrs();
   // One batched sweep launch (persistent grid chosen by the caller).
   // twisted: two-segment SPIKE variant (mass / derivative modes, sweep_tw.cuh).
   static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode, bool twisted);

@@ -595,3 +595,38 @@ def test_tma_and_legacy_sweeps_full_steps(knobs):
         for n, p in [(34, 2), (29, 3)]:
             errs, _ = _parity_run(n, p, 0.01, 3, material="phantom4")
             assert max(errs) <= TOL_STEP, (n, p, errs)
+
+
+@pytest.mark.parametrize("n,p", [(34, 2), (62, 2), (33, 3), (35, 1), (70, 2)])
+@pytest.mark.parametrize("s", [1, 2])
+def test_rhs_e_fused(n, p, s):  # (p = 1 runs the per-component cp.async kernel)
+    """The fused three-component RHS_E kernel (rhs3.cuh: one TMA pass over the six fields, per-
+    (component, scale) z accumulators; used for p <= 3 and even N >= 32 + 2p) against the oracle's
+    literal Kronecker sums, random per-test-function eps and mu, with a point source on E3;
+    several tiles incl. rim tiles, several z-chunks."""
+    O, G = both(n, p, 0.05)
+    N = n + p
+    eps = workloads.random_tf(N, 5, 1.0, 80.0)
+    mu = workloads.random_tf(N, 6, 0.5, 2.0)
+    O.set_materials_tf(eps, mu)
+    G.set_materials_tf(eps, mu)
+    f = workloads.random_fields(N, 7)
+    O.set_fields(f)
+    G.set_fields(f)
+    sig = np.full(4, 0.7)
+    pos = workloads.dipole_position(n)
+    O.set_source([None, None, O.point_load(*pos)], sig)
+    G.set_point_source(2, pos, sig)
+    Ro, Rg = O.rhs_e(s), G.rhs_e(s)
+    for d in range(3):
+        assert rel(Rg[d], Ro[d]) <= 1e-13, (d, rel(Rg[d], Ro[d]))
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_rhs_full_steps(fused):
+    """Full steps with the fused RHS_E (default) and the per-component kernels (ADI_RHS3=0) both
+    match the oracle (N = 36 and 66, p = 2; N = 36, p = 3; phantom material, source)."""
+    with _env(ADI_RHS3=fused):
+        for n, p in [(34, 2), (64, 2), (33, 3)]:
+            errs, _ = _parity_run(n, p, 0.01, 3, material="phantom4", source="modsine")
+            assert max(errs) <= TOL_STEP, (n, p, errs)
