@@ -159,6 +159,34 @@ adi_status adi_step(adi_patch patch, int64_t k);
  * ADI_ERR_ARG for other values. */
 adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
 
+/* NEXT-1 (the linear cost of banded direction solves): how a
+ * distributed patch solves its CONSTANT sweeps along the partitioned axis z (the mass sweeps of
+ * the E solves, a2/a6, and the M^{-1} of the uniform-mu derivative projections, a3/a4, a7/a8):
+ *   1 (default): partitioned (SPIKE) solve in place on the z-slabs -- each rank solves its
+ *      diagonal block of the banded matrix, the ranks all-gather 2p interface values per fiber
+ *      (instead of the fiber), and every rank finishes with the precomputed rows of the
+ *      2pR x 2pR interface system (adi_zsolve_tables); the row-modified z sweep (per-fiber
+ *      matrix) keeps the transposes;
+ *   0: every z sweep between all-to-all transposes (the per-fiber arithmetic of a whole patch:
+ *      bit-identical for any number of ranks).
+ * *active (may be NULL) = 1 if mode 1 is in effect: a distributed patch whose every rank holds
+ * >= 2p active rows of both PEC ranges.  ADI_ERR_ARG for other modes. */
+adi_status adi_set_zsolve(adi_patch patch, int32_t mode, int32_t* active);
+
+/* Host-only (no device): the tables of the partitioned z-solve for rank `rank` of `nranks`
+ * (rows of the axis split as adi_layout splits z) of the 1D mass matrix of (n, p) restricted to
+ * the active rows [lo, hi) (D1: [0, N) or [1, N-1)).  Outputs (caller-allocated, N = n + p):
+ *   *g0, *m: first active row of the rank and its number of active rows;
+ *   fac: m x (2p+1) banded LU (no pivoting) of the diagonal block A_r: per row l_{k,k-1-q}
+ *        (q < p), 1 / u_kk, u_{k,k+1+q};
+ *   tw:  2p x m, rows 0..p-1 and m-p..m-1 of A_r^{-1} (the tips of y = A_r^{-1} f);
+ *   cb:  2 p x p: the coupling C_r (rows g0.., columns g0-p..) then B_r (rows g0+m-p.., columns g0+m..);
+ *   q:   2p x 2p nranks: rows of K^{-1} (K: the interface system over the tips [t_s, b_s]_s) giving
+ *        t_{r+1} (rows 0..p-1) and b_{r-1} (rows p..2p-1), zero where the neighbour is absent.
+ * ADI_ERR_ARG: bad sizes, a rank with fewer than 2p active rows, or a singular block. */
+adi_status adi_zsolve_tables(int32_t n, int32_t p, int32_t nranks, int32_t rank, int32_t lo, int32_t hi, int32_t* g0,
+                             int32_t* m, double* fac, double* tw, double* cb, double* q);
+
 /* On-device diagnostic: out[c] = f_c^T (M (x) M (x) M) f_c for the six
  * fields and out[6] = 1/2 sum_c out[c], the discrete M-norm energy 1/2 (e^T M e + h^T M h)
  * (conserved by the curl part of the scheme).  Synchronises.  Whole patches only. */

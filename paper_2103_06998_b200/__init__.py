@@ -40,7 +40,7 @@ EXPORTS = [
     "adi_debug_rhs_h", "adi_debug_solve_e",
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
     "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA", "adi_divergence",
-    "adi_nccl_unique_id", "adi_loopback_create", "adi_loopback_destroy",
+    "adi_nccl_unique_id", "adi_loopback_create", "adi_loopback_destroy", "adi_set_zsolve", "adi_zsolve_tables",
 ]
 
 
@@ -156,6 +156,8 @@ def lib():
             L.adi_loopback_create.argtypes = [C.c_int32, C.POINTER(C.c_void_p)]
             L.adi_loopback_destroy.argtypes = [C.c_void_p]
             L.adi_loopback_destroy.restype = None
+            L.adi_set_zsolve.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
+            L.adi_zsolve_tables.argtypes = [C.c_int32] * 6 + [C.POINTER(C.c_int32)] * 2 + [C.c_void_p] * 4
             _lib = L
         return _lib
 
@@ -353,6 +355,13 @@ class Patch:
         """0: stiffened axis first (D7, default); 1: paper-literal x -> y -> z (V1)."""
         self._check(self._L.adi_set_sweep_order(self.h, int(order)))
 
+    def set_zsolve(self, mode: int) -> bool:
+        """NEXT-1: 1 (default) partitioned (SPIKE) z-solve of the constant sweeps of a distributed
+        patch; 0: every z sweep between transposes.  Returns whether the partitioned solve is in effect."""
+        act = C.c_int32(0)
+        self._check(self._L.adi_set_zsolve(self.h, int(mode), C.byref(act)))
+        return bool(act.value)
+
     def energy(self):
         """(per-field f^T M^3 f [6], M-norm energy 1/2 sum) -- on-device diagnostic."""
         out = (C.c_double * 7)()
@@ -481,3 +490,24 @@ class Patch:
         en = [_as_f64(x) for x in En]
         self._check(self._L.adi_debug_rhs_h(self.h, int(s), _ptr_array(eo), _ptr_array(en), _ptr_array(G)))
         return G
+
+
+def zsolve_tables(n: int, p: int, nranks: int, rank: int, lo: int, hi: int):
+    """Host tables of the NEXT-1 partitioned z-solve (adi_zsolve_tables; no device needed):
+    dict(g0, m, fac [m, 2p+1], tw [2p, m], C [p, p], B [p, p], q [2p, 2p nranks])."""
+    L = lib()
+    N = n + p
+    W = 2 * p + 1
+    fac = np.zeros(N * W)
+    tw = np.zeros(2 * p * N)
+    cb = np.zeros(2 * p * p)
+    q = np.zeros(2 * p * 2 * p * nranks)
+    g0, m = C.c_int32(0), C.c_int32(0)
+    st = L.adi_zsolve_tables(n, p, nranks, rank, lo, hi, C.byref(g0), C.byref(m), fac.ctypes.data, tw.ctypes.data,
+                             cb.ctypes.data, q.ctypes.data)
+    if st != ADI_OK:
+        raise AdiError(st, L.adi_last_error().decode())
+    mm = m.value
+    return dict(g0=g0.value, m=mm, fac=fac[:mm * W].reshape(mm, W).copy(), tw=tw[:2 * p * mm].reshape(2 * p, mm).copy(),
+                C=cb[:p * p].reshape(p, p).copy(), B=cb[p * p:].reshape(p, p).copy(),
+                q=q.reshape(2 * p, 2 * p * nranks).copy())

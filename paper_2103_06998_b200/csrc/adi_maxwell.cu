@@ -234,6 +234,16 @@ struct adi_patch_s {
   double* cy = nullptr;         // c in the y-slab layout
   double* xbuf[2] = {};         // pack / unpack buffers of the transposes (3 z-slabs each)
   Transport* tr = nullptr;
+  // NEXT-1 partitioned z-solve (spike.cuh) of the constant sweeps along z (mass sweeps, the M^{-1}
+  // of the derivative projections): zsolve 1 (default where every rank holds >= 2p active rows of
+  // both PEC variants) replaces their transposes by a 2p-value-per-fiber all-gather; 0: transposes
+  int zsolve = 1;
+  bool zspike_ok = false;
+  double* d_zsp[2] = {nullptr, nullptr};   // per variant: fac | tw | cb | q
+  int zsp_g0l[2] = {0, 0}, zsp_m[2] = {0, 0};
+  size_t zsp_off[2][4] = {};
+  double* ztips = nullptr;  // [3][2p][N^2]
+  double* zgath = nullptr;  // [R][3][2p][N^2]
 };
 
 // Exchanges of the distributed (slab) mode; implementations below (NCCL, in-process loopback)
@@ -246,6 +256,9 @@ struct Transport {
   virtual adi_status z2y(adi_patch P, double* const* src, double* const* dst, int nf) = 0;
   // y-slabs src[q] -> inner planes of the halo'd z-slabs dst[q]
   virtual adi_status y2z(adi_patch P, double* const* src, double* const* dst, int nf) = 0;
+  // recv[t * count + i] = rank t's send[i] (every rank, itself included): the interface tips of the
+  // partitioned z-solve (NEXT-1, spike.cuh)
+  virtual adi_status allgather(adi_patch P, const double* send, double* recv, int64_t count) = 0;
 };
 
 namespace {
@@ -875,6 +888,133 @@ adi_status full_step(adi_patch P) {
 // ===========================================================================
 int64_t slab_lo(int N, int R, int r) { return (int64_t)r * N / R; }
 
+// ---- NEXT-1: tables of the partitioned (SPIKE) solve along z (spike.cuh) ----
+// Dense solve with partial pivoting of the n x n system X Z = Bm (m right-hand sides, row-major).
+bool dense_lu_solve(std::vector<double> X, int n, std::vector<double>& Bm, int m) {
+  for (int c = 0; c < n; c++) {
+    int piv = c;
+    for (int r = c + 1; r < n; r++)
+      if (std::fabs(X[(size_t)r * n + c]) > std::fabs(X[(size_t)piv * n + c])) piv = r;
+    if (!(std::fabs(X[(size_t)piv * n + c]) > 0.0)) return false;
+    if (piv != c) {
+      for (int j = 0; j < n; j++) std::swap(X[(size_t)c * n + j], X[(size_t)piv * n + j]);
+      for (int j = 0; j < m; j++) std::swap(Bm[(size_t)c * m + j], Bm[(size_t)piv * m + j]);
+    }
+    for (int r = c + 1; r < n; r++) {
+      const double l = X[(size_t)r * n + c] / X[(size_t)c * n + c];
+      if (l == 0.0) continue;
+      for (int j = c; j < n; j++) X[(size_t)r * n + j] -= l * X[(size_t)c * n + j];
+      for (int j = 0; j < m; j++) Bm[(size_t)r * m + j] -= l * Bm[(size_t)c * m + j];
+    }
+  }
+  for (int c = n - 1; c >= 0; c--)
+    for (int j = 0; j < m; j++) {
+      double s = Bm[(size_t)c * m + j];
+      for (int k = c + 1; k < n; k++) s -= X[(size_t)c * n + k] * Bm[(size_t)k * m + j];
+      Bm[(size_t)c * m + j] = s / X[(size_t)c * n + c];
+    }
+  return true;
+}
+
+struct ZSpikeTab {
+  int g0 = 0, m = 0;        // first active row of the rank (global), active rows
+  std::vector<double> fac;  // m x W banded LU of A_r (mass_factor layout)
+  std::vector<double> tw;   // 2p x m: rows 0..p-1, m-p..m-1 of A_r^{-1}
+  std::vector<double> cb;   // C_r (p x p), B_r (p x p)
+  std::vector<double> q;    // 2p x 2pR: rows of K^{-1} for t_{r+1} (0..p-1) and b_{r-1} (p..2p-1)
+};
+
+// Rank r of R owns the rows [slab_lo(r), slab_lo(r+1)) of the axis; the system is X restricted
+// to [lo, hi) (PEC, D1).  Every rank needs >= 2p active rows (else false: the caller keeps the
+// transposes).  Interface unknowns xi = [t_0, b_0, t_1, b_1, ...] (top / bottom p rows per rank):
+//   t_s + V_s^top t_{s+1} + W_s^top b_{s-1} = y_s^top,  b_s + V_s^bot t_{s+1} + W_s^bot b_{s-1} = y_s^bot
+// with V_s = A_s^{-1} [0; B_s], W_s = A_s^{-1} [C_s; 0].
+bool mass_factor(const std::vector<double>& M, int N, int p, int lo, int hi, std::vector<double>& fac);
+
+bool zspike_tables(const std::vector<double>& X, int N, int p, int R, int r, int lo, int hi, ZSpikeTab& T,
+                   std::string& why) {
+  const int W = 2 * p + 1, nK = 2 * p * R;
+  std::vector<int> g0(R), m(R);
+  for (int s = 0; s < R; s++) {
+    g0[s] = std::max<int>((int)slab_lo(N, R, s), lo);
+    m[s] = std::min<int>((int)slab_lo(N, R, s + 1), hi) - g0[s];
+    if (m[s] < 2 * p) {
+      why = "a rank holds fewer than 2p active rows";
+      return false;
+    }
+  }
+  std::vector<double> K((size_t)nK * nK, 0.0);
+  for (int i = 0; i < nK; i++) K[(size_t)i * nK + i] = 1.0;
+  for (int s = 0; s < R; s++) {
+    const int ms = m[s], a = g0[s], b = a + ms;
+    std::vector<double> As((size_t)ms * ms);
+    for (int i = 0; i < ms; i++)
+      for (int j = 0; j < ms; j++) As[(size_t)i * ms + j] = X[(size_t)(a + i) * N + a + j];
+    // right-hand sides: [0; B_s] (columns 0..p-1), [C_s; 0] (columns p..2p-1)
+    std::vector<double> rhs((size_t)ms * 2 * p, 0.0);
+    for (int i = 0; i < p; i++)
+      for (int j = 0; j < p; j++) {
+        if (s + 1 < R) rhs[(size_t)(ms - p + i) * 2 * p + j] = X[(size_t)(b - p + i) * N + b + j];
+        if (s > 0) rhs[(size_t)i * 2 * p + p + j] = X[(size_t)(a + i) * N + a - p + j];
+      }
+    if (!dense_lu_solve(As, ms, rhs, 2 * p)) {
+      why = "singular diagonal block";
+      return false;
+    }
+    for (int i = 0; i < 2 * p; i++) {
+      const int lr = i < p ? i : ms - 2 * p + i;  // local row of tip i
+      const int row = 2 * p * s + i;
+      for (int j = 0; j < p; j++) {
+        if (s + 1 < R) K[(size_t)row * nK + 2 * p * (s + 1) + j] += rhs[(size_t)lr * 2 * p + j];
+        if (s > 0) K[(size_t)row * nK + 2 * p * (s - 1) + p + j] += rhs[(size_t)lr * 2 * p + p + j];
+      }
+    }
+    if (s != r) continue;
+    T.g0 = a, T.m = ms;
+    std::vector<double> fac;
+    if (!mass_factor(X, N, p, a, b, fac)) {
+      why = "tiny pivot in the banded LU of the diagonal block";
+      return false;
+    }
+    T.fac.assign(fac.begin(), fac.begin() + (size_t)ms * W);
+    // tip weights: rows of A_s^{-1} = columns of A_s^{-T}
+    std::vector<double> At((size_t)ms * ms), E((size_t)ms * 2 * p, 0.0);
+    for (int i = 0; i < ms; i++)
+      for (int j = 0; j < ms; j++) At[(size_t)i * ms + j] = As[(size_t)j * ms + i];
+    for (int i = 0; i < 2 * p; i++) E[(size_t)(i < p ? i : ms - 2 * p + i) * 2 * p + i] = 1.0;
+    if (!dense_lu_solve(At, ms, E, 2 * p)) {
+      why = "singular diagonal block";
+      return false;
+    }
+    T.tw.assign((size_t)2 * p * ms, 0.0);
+    for (int i = 0; i < 2 * p; i++)
+      for (int k = 0; k < ms; k++) T.tw[(size_t)i * ms + k] = E[(size_t)k * 2 * p + i];
+    T.cb.assign((size_t)2 * p * p, 0.0);
+    for (int i = 0; i < p; i++)
+      for (int j = 0; j < p; j++) {
+        if (s > 0) T.cb[(size_t)i * p + j] = X[(size_t)(a + i) * N + a - p + j];
+        if (s + 1 < R) T.cb[(size_t)p * p + i * p + j] = X[(size_t)(b - p + i) * N + b + j];
+      }
+  }
+  // rows of K^{-1} that rank r needs: solve K^T Z = e_rows
+  std::vector<double> Kt((size_t)nK * nK), Z((size_t)nK * 2 * p, 0.0);
+  for (int i = 0; i < nK; i++)
+    for (int j = 0; j < nK; j++) Kt[(size_t)i * nK + j] = K[(size_t)j * nK + i];
+  for (int j = 0; j < p; j++) {
+    if (r + 1 < R) Z[(size_t)(2 * p * (r + 1) + j) * 2 * p + j] = 1.0;
+    if (r > 0) Z[(size_t)(2 * p * (r - 1) + p + j) * 2 * p + p + j] = 1.0;
+  }
+  if (!dense_lu_solve(Kt, nK, Z, 2 * p)) {
+    why = "singular interface system";
+    return false;
+  }
+  T.q.assign((size_t)2 * p * nK, 0.0);
+  for (int i = 0; i < 2 * p; i++)
+    for (int c = 0; c < nK; c++) T.q[(size_t)i * nK + c] = Z[(size_t)c * 2 * p + i];
+  return true;
+}
+
+
 // 3D strided box copy on the patch stream (the pack / unpack of the transposes)
 adi_status box_copy(adi_patch P, double* dst, int64_t dx, int64_t dy, int64_t ox, int64_t oy, int64_t oz,
                     const double* src, int64_t sx, int64_t sy, int64_t px, int64_t py, int64_t pz, int64_t ex,
@@ -1011,6 +1151,19 @@ struct NcclTransport : Transport {
     }
     return ADI_OK;
   }
+  adi_status allgather(adi_patch P, const double* send, double* recv, int64_t count) override {
+    const NcclApi& A = nccl_api();
+    CUDA_TRY(cudaMemcpyAsync(recv + (int64_t)P->rank * count, send, count * sizeof(double), cudaMemcpyDeviceToDevice,
+                             P->stream));
+    NCCL_TRY(A.GroupStart());
+    for (int t = 0; t < P->nrk; t++) {
+      if (t == P->rank) continue;
+      NCCL_TRY(A.Send(send, count, ncclDouble, t, comm, P->stream));
+      NCCL_TRY(A.Recv(recv + (int64_t)t * count, count, ncclDouble, t, comm, P->stream));
+    }
+    NCCL_TRY(A.GroupEnd());
+    return ADI_OK;
+  }
 };
 
 // ---- in-process loopback: R patches driven by R host threads on one device ----
@@ -1115,9 +1268,70 @@ struct LoopTransport : Transport {
       return ADI_OK;
     });
   }
+  adi_status allgather(adi_patch P, const double* send, double* recv, int64_t count) override {
+    double* mine[1] = {const_cast<double*>(send)};
+    return exchange(P, mine, [&]() -> adi_status {
+      for (int t = 0; t < P->nrk; t++)
+        CUDA_TRY(cudaMemcpyAsync(recv + (int64_t)t * count, g->post[t][0], count * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, P->stream));
+      return ADI_OK;
+    });
+  }
 };
 
 double* slab_inner(adi_patch P, double* f) { return f + (int64_t)P->p * P->N * P->N; }
+
+// NEXT-1: the z jobs of a mass / derivative-projection stage solved in
+// place on the z-slabs by the partitioned (SPIKE) solve of spike.cuh: a tip pass, one all-gather of
+// 2p values per fiber and rank, and the corrected segment solve.  No transposes.
+adi_status zsolve_spike(adi_patch P, int mode, const SweepReq* zj, int nzj) {
+  const int p = P->p;
+  const int64_t NN = (int64_t)P->N * P->N;
+  adi_status st;
+  if (mode == adi::SW_DER) {  // A u along z reads p planes beyond the slab: refresh the inputs' halos
+    double* f[3];
+    for (int q = 0; q < nzj; q++) f[q] = const_cast<double*>(zj[q].in) - (int64_t)p * NN;
+    if ((st = P->tr->halo(P, f, nzj))) return st;
+  }
+  adi::SpikeBatch B{};
+  B.NN = NN, B.nz = P->nz, B.njobs = nzj, B.R = P->nrk, B.N = P->N, B.k0 = P->k0;
+  for (int v = 0; v < 2; v++) {
+    if (!P->d_zsp[v]) continue;
+    adi::SpikeTabDev& T = B.tab[v];
+    T.fac = P->d_zsp[v] + P->zsp_off[v][0];
+    T.tw = P->d_zsp[v] + P->zsp_off[v][1];
+    T.cb = P->d_zsp[v] + P->zsp_off[v][2];
+    T.q = P->d_zsp[v] + P->zsp_off[v][3];
+    T.g0l = P->zsp_g0l[v], T.m = P->zsp_m[v];
+  }
+  B.Ab = P->d_tab + (size_t)adi::OP_A * P->N * P->W;
+  B.tips = P->ztips;
+  B.gath = P->zgath;
+  for (int q = 0; q < nzj; q++) {
+    adi::SpikeJob& J = B.job[q];
+    int lo, hi;
+    active_range(P, zj[q].comp, 2, lo, hi);
+    J.v = lo == 0 ? 0 : 1;
+    if (!P->d_zsp[J.v]) return fail(ADI_ERR_STATE, "z-spike: no tables for the PEC range of component %d", zj[q].comp);
+    J.in = zj[q].in;
+    J.out = zj[q].out;
+    J.der = mode == adi::SW_DER;
+    J.base = zj[q].base;
+    J.coef = zj[q].coef;
+    J.gbuf = (J.der && zj[q].out == zj[q].base) ? P->Y[q] : zj[q].out;
+  }
+  const int cls = mode == adi::SW_DER ? ADI_K_SWEEP_DER : ADI_K_SWEEP_MASS;
+  {
+    LaunchScope ls(P, cls);
+    with_degree(p, [&](auto ops) { ops.spike(P->stream, B, 0); });
+    CUDA_TRY(cudaGetLastError());
+  }
+  if ((st = P->tr->allgather(P, P->ztips, P->zgath, (int64_t)nzj * 2 * p * NN))) return st;
+  LaunchScope ls(P, cls);
+  with_degree(p, [&](auto ops) { ops.spike(P->stream, B, 1); });
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
 
 // One stage of sweeps in slab mode: x / y jobs on the z-slabs, z jobs on y-slabs between one
 // batched z -> y transpose of their inputs (DER: u and base) and one y -> z transpose back.
@@ -1142,6 +1356,7 @@ adi_status dist_sweeps(adi_patch P, int mode, const SweepReq* jobs, int nj, cons
   adi_status st;
   if (nl && (st = launch_sweeps(P, loc, nl, mode))) return st;
   if (!nzj) return ADI_OK;
+  if (mode != adi::SW_MOD && P->zsolve == 1 && P->zspike_ok) return zsolve_spike(P, mode, zj, nzj);
   // transpose in: inputs (and DER bases) -> Y
   double* src[3];
   double* dst[3];
@@ -1285,6 +1500,49 @@ adi_status dist_substep(adi_patch P, int s) {
 }
 
 // host band tables and mass factorisations ----------------------------------
+// The 1D Galerkin matrices as every kernel uses them (host, dense N x N): Gauss assembly
+// (D4, D11), interior rows made exactly Toeplitz, persymmetry imposed.
+void host_matrices(int n, int p, std::vector<double>& M, std::vector<double>& S, std::vector<double>& A) {
+  const int N = n + p;
+  Space1D sp(n, p);
+  assemble_1d(sp, M, S, A);
+  // Uniform knots make rows [2p, N-2p) of M, S, A translates of one stencil
+  // (P:429-440); quadrature at shifted points leaves them equal only to
+  // ~1e-16 relative.  Copy the middle row's stencil into every interior row so
+  // that the interior is exactly Toeplitz: the kernels then take interior
+  // coefficients and the converged interior LU factors from the parameter
+  // bank (a rounding-level change of the matrices).
+  if (N > 4 * p) {
+    const int mid = N / 2;
+    // the interior stencil is symmetric (M, S) / antisymmetric (A); make the copied row exactly so
+    for (int q = 1; q <= p; q++) {
+      const size_t r = (size_t)mid * N + mid;
+      M[r - q] = M[r + q];
+      S[r - q] = S[r + q];
+      A[r - q] = -A[r + q];
+    }
+    A[(size_t)mid * N + mid] = 0.0;
+    for (std::vector<double>* X : {&M, &S, &A})
+      for (int r = 2 * p; r < N - 2 * p; r++)
+        for (int q = -p; q <= p; q++) (*X)[(size_t)r * N + r + q] = (*X)[(size_t)mid * N + mid + q];
+  }
+  // The basis is symmetric under x -> 1 - x (B_i(1-x) = B_{N-1-i}(x)), so M and S are
+  // persymmetric and A anti-persymmetric: X[N-1-i][N-1-j] = +-X[i][j].  Mirror the top
+  // rows onto the bottom ones (again a rounding-level change) so that the twisted
+  // sweeps can solve the bottom half-fiber with the top half's LU factors.
+  for (int i = 0; i < N; i++) {
+    const int ii = N - 1 - i;
+    if (ii <= i) break;
+    for (int q = -p; q <= p; q++) {
+      const int j = i + q, jj = N - 1 - j;
+      if (j < 0 || j >= N) continue;
+      M[(size_t)ii * N + jj] = M[(size_t)i * N + j];
+      S[(size_t)ii * N + jj] = S[(size_t)i * N + j];
+      A[(size_t)ii * N + jj] = -A[(size_t)i * N + j];
+    }
+  }
+}
+
 void band_from_dense(const std::vector<double>& X, bool transpose, int N, int p, int lo, int hi, double* out) {
   const int W = 2 * p + 1;
   for (int r = 0; r < N; r++)
@@ -1578,6 +1836,7 @@ void adi_destroy(adi_patch P) {
   for (int i = 0; i < 6; i++) f(P->iu[i]);
   for (int i = 0; i < 6; i++) f(P->Y[i]);
   f(P->cy), f(P->xbuf[0]), f(P->xbuf[1]);
+  f(P->d_zsp[0]), f(P->d_zsp[1]), f(P->ztips), f(P->zgath);
   if (P->tr) {
     if (auto* L = dynamic_cast<LoopTransport*>(P->tr)) {
       std::lock_guard<std::mutex> lk(L->g->m);
@@ -1649,42 +1908,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     P->use_tma = p >= 2 && (N % 2 == 0) && N >= adi::RX_TX + 2 * p && tma_encoder() != nullptr && !(s && atoi(s));
   }
   Space1D sp(P->n, p);
-  assemble_1d(sp, P->M, P->S, P->A);
-  // Uniform knots make rows [2p, N-2p) of M, S, A translates of one stencil
-  // (P:429-440); quadrature at shifted points leaves them equal only to
-  // ~1e-16 relative.  Copy the middle row's stencil into every interior row so
-  // that the interior is exactly Toeplitz: the kernels then take interior
-  // coefficients and the converged interior LU factors from the parameter
-  // bank (a rounding-level change of the matrices).
-  if (N > 4 * p) {
-    const int mid = N / 2;
-    // the interior stencil is symmetric (M, S) / antisymmetric (A); make the copied row exactly so
-    for (int q = 1; q <= p; q++) {
-      const size_t r = (size_t)mid * N + mid;
-      P->M[r - q] = P->M[r + q];
-      P->S[r - q] = P->S[r + q];
-      P->A[r - q] = -P->A[r + q];
-    }
-    P->A[(size_t)mid * N + mid] = 0.0;
-    for (std::vector<double>* X : {&P->M, &P->S, &P->A})
-      for (int r = 2 * p; r < N - 2 * p; r++)
-        for (int q = -p; q <= p; q++) (*X)[(size_t)r * N + r + q] = (*X)[(size_t)mid * N + mid + q];
-  }
-  // The basis is symmetric under x -> 1 - x (B_i(1-x) = B_{N-1-i}(x)), so M and S are
-  // persymmetric and A anti-persymmetric: X[N-1-i][N-1-j] = +-X[i][j].  Mirror the top
-  // rows onto the bottom ones (again a rounding-level change) so that the twisted
-  // sweeps can solve the bottom half-fiber with the top half's LU factors.
-  for (int i = 0; i < N; i++) {
-    const int ii = N - 1 - i;
-    if (ii <= i) break;
-    for (int q = -p; q <= p; q++) {
-      const int j = i + q, jj = N - 1 - j;
-      if (j < 0 || j >= N) continue;
-      P->M[(size_t)ii * N + jj] = P->M[(size_t)i * N + j];
-      P->S[(size_t)ii * N + jj] = P->S[(size_t)i * N + j];
-      P->A[(size_t)ii * N + jj] = -P->A[(size_t)i * N + j];
-    }
-  }
+  host_matrices(P->n, p, P->M, P->S, P->A);
   // material weights (D6): w[r*n+e] = int_{elem e} B_r / int B_r (Gauss q = p+1, exact)
   {
     P->wmat.assign((size_t)N * P->n, 0.0);
@@ -1818,6 +2042,33 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
       P->tr = T;
       std::lock_guard<std::mutex> lk(G->m);
       G->patch[P->rank] = P;
+    }
+    // NEXT-1: partitioned z-solve tables (variant 0: rows [0, N); 1: the PEC range [1, N-1))
+    {
+      bool ok = true;
+      std::string why;
+      for (int v = 0; v < 2 && ok; v++) {
+        if (v == 1 && cfg->bc != ADI_BC_PEC) break;
+        ZSpikeTab T;
+        if (!zspike_tables(P->M, N, p, P->nrk, P->rank, v, v ? N - 1 : N, T, why)) {
+          ok = false;
+          break;
+        }
+        const size_t n0 = T.fac.size(), n1 = T.tw.size(), n2 = T.cb.size(), n3 = T.q.size();
+        if (!dmalloc(&P->d_zsp[v], n0 + n1 + n2 + n3)) return bail(fail(ADI_ERR_OOM, "cudaMalloc z-spike tables"));
+        P->zsp_off[v][0] = 0, P->zsp_off[v][1] = n0, P->zsp_off[v][2] = n0 + n1, P->zsp_off[v][3] = n0 + n1 + n2;
+        std::vector<double> all;
+        for (auto* X : {&T.fac, &T.tw, &T.cb, &T.q}) all.insert(all.end(), X->begin(), X->end());
+        if (cudaMemcpy(P->d_zsp[v], all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+          return bail(fail(ADI_ERR_CUDA, "z-spike tables upload"));
+        P->zsp_g0l[v] = T.g0 - P->k0, P->zsp_m[v] = T.m;
+      }
+      if (ok) {
+        const size_t per = (size_t)3 * 2 * p * N * N;
+        if (!dmalloc(&P->ztips, per) || !dmalloc(&P->zgath, per * P->nrk))
+          return bail(fail(ADI_ERR_OOM, "cudaMalloc z-spike exchange buffers"));
+      }
+      P->zspike_ok = ok;
     }
   }
   const size_t U = whole ? (size_t)P->U : 0;
@@ -2457,6 +2708,36 @@ adi_status adi_set_sweep_order(adi_patch P, int32_t order) {
   if (order != 0 && order != 1) return fail(ADI_ERR_ARG, "adi_set_sweep_order: order %d not 0 or 1", order);
   drop_graph(P);
   P->sweep_order = order;
+  return ADI_OK;
+}
+
+adi_status adi_set_zsolve(adi_patch P, int32_t mode, int32_t* active) {
+  CHECK_PATCH(P);
+  if (mode != 0 && mode != 1) return fail(ADI_ERR_ARG, "adi_set_zsolve: mode %d not 0 or 1", mode);
+  drop_graph(P);
+  P->zsolve = mode;
+  if (active) *active = P->slab && P->nrk > 1 && mode == 1 && P->zspike_ok ? 1 : 0;
+  return ADI_OK;
+}
+
+adi_status adi_zsolve_tables(int32_t n, int32_t p, int32_t nranks, int32_t rank, int32_t lo, int32_t hi, int32_t* g0,
+                             int32_t* m, double* fac, double* tw, double* cb, double* q) {
+  if (n < 1 || p < 1 || p > 5) return fail(ADI_ERR_ARG, "adi_zsolve_tables: n = %d, p = %d", n, p);
+  const int N = n + p;
+  if (nranks < 1 || nranks > N || rank < 0 || rank >= nranks)
+    return fail(ADI_ERR_ARG, "adi_zsolve_tables: rank %d of %d", rank, nranks);
+  if (lo < 0 || hi > N || hi - lo < 1) return fail(ADI_ERR_ARG, "adi_zsolve_tables: range [%d, %d)", lo, hi);
+  if (!g0 || !m || !fac || !tw || !cb || !q) return fail(ADI_ERR_ARG, "adi_zsolve_tables: NULL output");
+  std::vector<double> M, S, A;
+  host_matrices(n, p, M, S, A);
+  ZSpikeTab T;
+  std::string why;
+  if (!zspike_tables(M, N, p, nranks, rank, lo, hi, T, why)) return fail(ADI_ERR_ARG, "adi_zsolve_tables: %s", why.c_str());
+  *g0 = T.g0, *m = T.m;
+  std::copy(T.fac.begin(), T.fac.end(), fac);
+  std::copy(T.tw.begin(), T.tw.end(), tw);
+  std::copy(T.cb.begin(), T.cb.end(), cb);
+  std::copy(T.q.begin(), T.q.end(), q);
   return ADI_OK;
 }
 

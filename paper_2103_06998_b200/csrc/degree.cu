@@ -33,6 +33,8 @@ template <>
 void Ops<ADI_P>::sweep_res(cudaStream_t, unsigned, unsigned, size_t, const SweepBatch&, const SweepResMaps&, int) {}
 template <>
 cudaError_t Ops<ADI_P>::sweep_res_attrs() { return cudaErrorNotSupported; }
+template <>
+void Ops<ADI_P>::spike(cudaStream_t, const SpikeBatch&, int) {}
 #else
 
 namespace {
@@ -183,6 +185,13 @@ template <>
 void Ops<ADI_P>::factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad,
                         double tol) {
   factor_kernel<ADI_P><<<grid, 128, 0, st>>>(B, iu, bad, tol);
+}
+
+template <>
+void Ops<ADI_P>::spike(cudaStream_t st, const SpikeBatch& B, int solve) {
+  const dim3 grid((unsigned)((B.NN + 255) / 256), (unsigned)B.njobs);
+  if (solve) spike_solve_kernel<ADI_P><<<grid, 256, 0, st>>>(B);
+  else spike_tips_kernel<ADI_P><<<grid, 256, 0, st>>>(B);
 }
 
 #endif  // ADI_STUB

@@ -13,6 +13,7 @@
 #include "sweep_tw.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_res.cuh"
+#include "spike.cuh"
 
 namespace adi {
 
@@ -43,6 +44,9 @@ struct Ops {
   static void sweep_res(cudaStream_t st, unsigned grid, unsigned warps, size_t smem, const SweepBatch& B,
                         const SweepResMaps& maps, int mode);
   static cudaError_t sweep_res_attrs();
+  // NEXT-1 partitioned z-solve (spike.cuh): solve = 0: tip pass, 1: corrected banded solve;
+  // grid (fiber blocks of 256, jobs).
+  static void spike(cudaStream_t st, const SpikeBatch& B, int solve);
   // Pivot cache of one row-modified family (job 0 of B).
   static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };

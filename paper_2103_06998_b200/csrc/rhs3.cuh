@@ -117,11 +117,21 @@ struct Rx3Geom {
 };
 
 template <int P>
-__host__ __device__ constexpr size_t rhs3_smem_bytes() {
+__host__ __device__ constexpr size_t rhs3_smem_bytes_n(int nsx) {
   using G = Rx3Geom<P>;
-  return sizeof(double) * ((size_t)RX_RING * 6 * G::PLANEP + (size_t)G::NXS * G::HY * RX_TX +
+  return sizeof(double) * ((size_t)RX_RING * 6 * G::PLANEP + (size_t)nsx * G::NXS * G::HY * RX_TX +
                            (size_t)3 * (RX_KCMAX + RX_TX + RX_TY) * (2 * P + 1)) +
          RX_RING * sizeof(uint64_t) + 1024;
+}
+// x-filtered buffers: two (the x-pass of plane k+1 overlaps the y/z-pass of plane k, one barrier
+// per plane) when they fit the 227 KB of shared memory a block may use, else one
+template <int P>
+__host__ __device__ constexpr int rhs3_nsx() {
+  return rhs3_smem_bytes_n<P>(2) <= 227u * 1024u ? 2 : 1;
+}
+template <int P>
+__host__ __device__ constexpr size_t rhs3_smem_bytes() {
+  return rhs3_smem_bytes_n<P>(rhs3_nsx<P>());
 }
 
 template <int P, int S, bool FAST>
@@ -131,9 +141,10 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
   constexpr int W = G::W, HX = G::HX, HY = G::HY, PLANE = G::PLANE, PLANEP = G::PLANEP;
   constexpr int NXS = Prog::nx();
   static_assert(NXS == G::NXS, "ten distinct (field, x-operator) pairs per substep");
+  constexpr int NSX = rhs3_nsx<P>();
   double* ring = smem;                                              // [RING][6][PLANEP]
-  double* sx = ring + RX_RING * 6 * PLANEP;                         // [NXS][HY][TX]
-  double* czs = sx + NXS * HY * RX_TX;                              // [3][KCMAX][W]
+  double* sx0 = ring + RX_RING * 6 * PLANEP;                        // [NSX][NXS][HY][TX]
+  double* czs = sx0 + NSX * NXS * HY * RX_TX;                       // [3][KCMAX][W]
   double* cxs = czs + 3 * RX_KCMAX * W;                             // [3][TX][W]
   double* cys = cxs + 3 * RX_TX * W;                                // [3][TY][W]
   uint64_t* bar = reinterpret_cast<uint64_t*>(cys + 3 * RX_TY * W);  // [RING]
@@ -250,6 +261,7 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
 #pragma unroll
           for (int d = 0; d < 3; d++) ld[d][r] = (ok && sval != 0.0 && args.load[d]) ? args.load[d][I] : 0.0;
         }
+        double* sx = sx0 + (NSX == 2 ? (it & 1) * (NXS * HY * RX_TX) : 0);
         mbar_wait(&bar[st], (unsigned)((it / RX_RING) & 1));
         // ---- x-pass: each field's rows read once, every x-operator of the field applied
         auto xpass = [&](auto kx) {
@@ -297,6 +309,22 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
         // Z[k][2P - jj] (row k of the band table); interior planes: the Toeplitz row
         const int kout0 = kin - P - zoff;  // output-local plane of jj = 0
         const bool zint = kg0 + kout0 >= 2 * P && kg0 + kout0 + 2 * P < N - 2 * P;
+        // z coefficients of this input plane, once per plane for the three z-operators M, A, B
+        // (the products below index them with compile-time operator and plane slot)
+        double zc[3][W];
+        if (zint) {
+#pragma unroll
+          for (int o = 0; o < 3; o++)
+#pragma unroll
+            for (int jj = 0; jj < W; jj++) zc[o][jj] = args.kint[o][2 * P - jj];
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < W; jj++) {
+            const int ko = min(max(kout0 + jj, k0), k1 - 1) - k0;
+#pragma unroll
+            for (int o = 0; o < 3; o++) zc[o][jj] = czs[(o * RX_KCMAX + ko) * W + 2 * P - jj];
+          }
+        }
         rx3_static_for<0, NXS>([&](auto xsc) {
           constexpr int xs = decltype(xsc)::value;
           double col[W + 1];
@@ -323,20 +351,13 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
               if constexpr (Prog::sign(t) < 0.0) vA = -vA, vB = -vB;
 #pragma unroll
               for (int jj = 0; jj < W; jj++) {
-                double zc;
-                if (zint) {
-                  zc = args.kint[zop][2 * P - jj];
-                } else {
-                  const int ko = min(max(kout0 + jj, k0), k1 - 1) - k0;
-                  zc = czs[(zop * RX_KCMAX + ko) * W + 2 * P - jj];
-                }
-                acc[g][jj][0] = fma(zc, vA, acc[g][jj][0]);
-                acc[g][jj][1] = fma(zc, vB, acc[g][jj][1]);
+                acc[g][jj][0] = fma(zc[zop][jj], vA, acc[g][jj][0]);
+                acc[g][jj][1] = fma(zc[zop][jj], vB, acc[g][jj][1]);
               }
             }
           });
         });
-        __syncthreads();  // sx consumed
+        if (NSX == 1) __syncthreads();  // sx consumed (two buffers: the next x-pass writes the other)
         // ---- output plane k = kin - P is complete
         {
           const int slotk = 0;

@@ -105,6 +105,15 @@ class Comm:
         for req in tdist.batch_isend_irecv(ops):
             req.wait()
 
+    # -- NEXT-1: interface tips of the partitioned z-solve ---------------------------
+    def allgather(self, t):
+        """[R, *t.shape]: every rank's t (the 2p tips per fiber of the partitioned z-solve)."""
+        if self.R == 1:
+            return t.unsqueeze(0).clone()
+        out = [torch.empty_like(t) for _ in range(self.R)]
+        tdist.all_gather(out, t.contiguous(), group=self.group)
+        return torch.stack(out)
+
     # -- transposes ---------------------------------------------------------------
     def z2y(self, src, dst, sendbuf):
         """src: own z-slab (nz, N, N) -> dst: own y-slab (N, ny, N)."""
@@ -160,7 +169,7 @@ class DistPatch:
     by default the library patch of this rank (CUDA; no other backend in the product)."""
 
     def __init__(self, n: int, p: int, tau: float, bc: int = 0, group=None, backend=None, device=None,
-                 rank: int | None = None, nranks: int | None = None, comm=None):
+                 rank: int | None = None, nranks: int | None = None, comm=None, zsolve: bool = False):
         if rank is None:
             if tdist is not None and tdist.is_available() and tdist.is_initialized():
                 rank, nranks = tdist.get_rank(group), tdist.get_world_size(group)
@@ -206,6 +215,15 @@ class DistPatch:
             # the buffers above were allocated and zero-filled on the current stream; every later
             # use is on self.stream, so order it after those fills
             self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        # NEXT-1 (opt-in here; the library's own distributed step defaults to it): mass sweeps and
+        # derivative projections along z by the partitioned solve (tables from adi_zsolve_tables;
+        # the backend provides spike_tips / spike_solve), no transposes for them
+        self.ztab = None
+        if zsolve:
+            import paper_2103_06998_b200 as adi
+            self.ztab = {0: adi.zsolve_tables(n, p, nranks, rank, 0, N)}
+            if bc == 0:
+                self.ztab[1] = adi.zsolve_tables(n, p, nranks, rank, 1, N - 1)
         self.set_materials_tf(torch.ones(N ** 3, dtype=torch.float64, device=self.device), None)
 
     def _on_stream(self):
@@ -316,6 +334,14 @@ class DistPatch:
         jobs_z: dicts with 'comp', 'in' (z-slab), 'out' (z-slab) [, 'iu', 'base', 'coef']."""
         if not jobs_z:
             return
+        if self.ztab is not None and mode != MOD:
+            if mode == DER:  # A u along z reads p planes beyond the slab
+                self.comm.halo_exchange([j["in_h"] for j in jobs_z])
+            for j in jobs_z:
+                j["v"] = 1 if (self.bc == 0 and j["comp"] < 2) else 0
+            tips = self.B.spike_tips(mode, jobs_z, self.ztab, self.k0)
+            self.B.spike_solve(mode, jobs_z, self.ztab, self.k0, self.comm.allgather(tips))
+            return
         jobs = []
         for q, j in enumerate(jobs_z):
             self.comm.z2y(j["in"], self.Y[q], self.sendbuf)
@@ -380,14 +406,14 @@ class DistPatch:
                 a1 = (d + 1) % 3 if s == 1 else (d + 2) % 3
                 x1 = (d + 2) % 3 if s == 1 else (d + 1) % 3
                 jobs.append(dict(axis=a1, comp=3 + d, **{"in": Eo[x1]}, out=self.inner(Gb[d]),
-                                 base=self.inner(F[3 + d]), coef=-b if s == 1 else b))
+                                 base=self.inner(F[3 + d]), coef=-b if s == 1 else b, in_h=F[x1]))
             self._sweeps(DER, jobs)
             jobs = []
             for d in range(3):
                 a2 = (d + 2) % 3 if s == 1 else (d + 1) % 3
                 x2 = (d + 1) % 3 if s == 1 else (d + 2) % 3
                 jobs.append(dict(axis=a2, comp=3 + d, **{"in": E_new[x2]}, out=self.inner(Gb[d]),
-                                 base=self.inner(Gb[d]), coef=b if s == 1 else -b))
+                                 base=self.inner(Gb[d]), coef=b if s == 1 else -b, in_h=Rb[x2]))
             self._sweeps(DER, jobs)
         else:
             # general mu: G from discrete2/discrete4 (needs halos of the new E), then M^-3

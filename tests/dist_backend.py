@@ -141,3 +141,52 @@ class CpuBoxBackend:
         o = out.numpy().reshape(sh)
         o[...] = res
         self.box_pec(comp, out, (N, N, nzout), (0, 0, kg0))
+
+    # -- NEXT-1: partitioned z-solve (restated from spike.cuh / adi_zsolve_tables) ------------
+    def _w(self, mode, j, T, k0):
+        """Right-hand side rows of the rank's active z-segment: f, or A u along z (halo'd u)."""
+        g0l, m, P = T["g0"] - k0, T["m"], self.p
+        if mode != 2:  # mass
+            return j["in"].numpy()[g0l:g0l + m].reshape(m, -1)
+        uh = j["in_h"].numpy().reshape(j["in_h"].shape[0], -1)  # planes -P .. nz+P-1
+        A = self.A
+        w = np.zeros((m, uh.shape[1]))
+        for k in range(m):
+            g = T["g0"] + k
+            for q in range(-P, P + 1):
+                if 0 <= g + q < self.N:
+                    w[k] += A[g, g + q] * uh[g0l + k + q + P]
+        return w
+
+    def spike_tips(self, mode, jobs, tabs, k0):
+        out = []
+        for j in jobs:
+            T = tabs[j["v"]]
+            out.append(T["tw"] @ self._w(mode, j, T, k0))
+        return torch.from_numpy(np.stack(out))  # [job, 2p, N*N]
+
+    def spike_solve(self, mode, jobs, tabs, k0, gath):
+        P = self.p
+        G = gath.numpy()  # [R, job, 2p, N*N]
+        for q, j in enumerate(jobs):
+            T = tabs[j["v"]]
+            g0l, m = T["g0"] - k0, T["m"]
+            tb = T["q"] @ G[:, q].reshape(-1, G.shape[-1])  # rows: t_{r+1} (P), b_{r-1} (P)
+            w = self._w(mode, j, T, k0).copy()
+            w[:P] -= T["C"] @ tb[P:]
+            w[m - P:] -= T["B"] @ tb[:P]
+            fac = T["fac"]
+            g = np.zeros_like(w)
+            for k in range(m):  # forward elimination (l_{k,k-1-q} = fac[k, q])
+                g[k] = w[k] - sum(fac[k, qq] * g[k - 1 - qq] for qq in range(P) if k - 1 - qq >= 0)
+            x = np.zeros_like(w)
+            for k in range(m - 1, -1, -1):  # back substitution (1/u_kk = fac[k, P], u_{k,k+1+q} = fac[k, P+1+q])
+                x[k] = (g[k] - sum(fac[k, P + 1 + qq] * x[k + 1 + qq] for qq in range(P) if k + 1 + qq < m)) * fac[k, P]
+            out = j["out"].numpy().reshape(j["out"].shape[0], -1)
+            if mode == 2:
+                base = j["base"].numpy().reshape(out.shape)[g0l:g0l + m].copy()
+                out[g0l:g0l + m] = base + j["coef"] * x
+            else:
+                out[g0l:g0l + m] = x
+            out[:g0l] = 0.0
+            out[g0l + m:] = 0.0

@@ -89,14 +89,14 @@ def test_comm_gloo(world, N, P):
     _run(_comm_worker, world, N, P)
 
 
-def _step_worker(rank, world, n, p, tau, steps, mu_kind, source, outdir):
+def _step_worker(rank, world, n, p, tau, steps, mu_kind, source, outdir, zsolve=False):
     from tests.dist_backend import CpuBoxBackend
 
     import workloads
 
     N = n + p
     be = CpuBoxBackend(n, p, tau)
-    D = DistPatch(n, p, tau, backend=be, rank=rank, nranks=world)
+    D = DistPatch(n, p, tau, backend=be, rank=rank, nranks=world, zsolve=zsolve)
     eps = workloads.element_eps(n, "random", seed=5)
     mu = None if mu_kind == "uniform" else workloads.element_eps(n, "random", seed=6) / 40.0
     D.set_materials(eps, mu)
@@ -110,15 +110,20 @@ def _step_worker(rank, world, n, p, tau, steps, mu_kind, source, outdir):
     np.save(os.path.join(outdir, f"r{rank}.npy"), np.stack([x.numpy() for x in D.get_fields()]))
 
 
-@pytest.mark.parametrize("world,n,p,mu_kind,source", [(2, 6, 2, "uniform", False), (2, 5, 3, "random", False),
-                                                      (3, 7, 2, "uniform", True)])
-def test_dist_step_gloo(tmp_path, world, n, p, mu_kind, source):
-    """Slab-decomposed step (world ranks, gloo) == oracle single-domain step, <= 1e-10."""
+@pytest.mark.parametrize("world,n,p,mu_kind,source,zsolve",
+                         [(2, 6, 2, "uniform", False, False), (2, 5, 3, "random", False, False),
+                          (3, 7, 2, "uniform", True, False),
+                          (2, 10, 2, "uniform", True, True), (3, 13, 2, "uniform", False, True),
+                          (2, 11, 3, "uniform", False, True)])
+def test_dist_step_gloo(tmp_path, world, n, p, mu_kind, source, zsolve):
+    """Slab-decomposed step (world ranks, gloo) == oracle single-domain step, <= 1e-10.
+    zsolve: NEXT-1 partitioned z-solve of the mass sweeps / derivative projections (tables from the
+    library's adi_zsolve_tables, tips all-gathered over gloo) instead of their transposes."""
     import oracle
     import workloads
 
     tau, steps = 0.02, 2
-    _run(_step_worker, world, n, p, tau, steps, mu_kind, source, str(tmp_path))
+    _run(_step_worker, world, n, p, tau, steps, mu_kind, source, str(tmp_path), zsolve)
     N = n + p
     got = np.concatenate([np.load(tmp_path / f"r{r}.npy") for r in range(world)], axis=1)  # [c, k, j, i]
     O = oracle.Patch(n, p, tau)
@@ -133,3 +138,59 @@ def test_dist_step_gloo(tmp_path, world, n, p, mu_kind, source):
         r = ref[c].reshape(N, N, N)
         err = np.linalg.norm(got[c] - r) / np.linalg.norm(r)
         assert err <= 1e-10, (c, err)
+
+
+def _zsolve_worker(rank, world, n, p, lo, hi):
+    """NEXT-1 host logic over gloo: each rank solves its diagonal block with the library's tables,
+    all-gathers 2p tips per fiber, corrects and finishes -- equal to the global banded solve."""
+    import paper_2103_06998_b200 as adi
+    import oracle
+
+    N = n + p
+    M = oracle.Patch(n, p, 0.01).matrices()[0]
+    rng = np.random.default_rng(7)
+    F = rng.uniform(-1, 1, size=(N, 40))  # 40 fibers, rows along the partitioned axis
+    T = adi.zsolve_tables(n, p, world, rank, lo, hi)
+    g0, m = T["g0"], T["m"]
+    assert (g0, g0 + m) == (max(rank * N // world, lo), min((rank + 1) * N // world, hi))
+    # tips of y = A_r^{-1} f: the tip weights are rows of the inverse of the diagonal block
+    Ar = M[g0:g0 + m, g0:g0 + m]
+    Ainv = np.linalg.inv(Ar)
+    assert np.allclose(T["tw"], np.concatenate([Ainv[:p], Ainv[m - p:]]), rtol=0, atol=1e-12 * abs(Ainv).max())
+    w = F[g0:g0 + m]
+    tips = torch.from_numpy(T["tw"] @ w)
+    out = [torch.empty_like(tips) for _ in range(world)]
+    dist.all_gather(out, tips)
+    tb = T["q"] @ torch.stack(out).numpy().reshape(-1, F.shape[1])
+    w = w.copy()
+    w[:p] -= T["C"] @ tb[p:]
+    w[m - p:] -= T["B"] @ tb[:p]
+    x = np.linalg.solve(Ar, w)
+    ref = np.linalg.solve(M[lo:hi, lo:hi], F[lo:hi])[g0 - lo:g0 - lo + m]
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+    # the banded LU factors of the block (no pivoting) reproduce A_r
+    fac = T["fac"]
+    L, U = np.eye(m), np.zeros((m, m))
+    for k in range(m):
+        for q in range(p):
+            if k - 1 - q >= 0:
+                L[k, k - 1 - q] = fac[k, q]
+        U[k, k] = 1.0 / fac[k, p]
+        for q in range(p):
+            if k + 1 + q < m:
+                U[k, k + 1 + q] = fac[k, p + 1 + q]
+    assert np.abs(L @ U - Ar).max() <= 1e-13 * np.abs(Ar).max()
+
+
+@pytest.mark.parametrize("world,n,p,lo_off", [(2, 10, 2, 0), (2, 10, 2, 1), (3, 13, 2, 1), (3, 16, 3, 0), (2, 11, 1, 1)])
+def test_zsolve_tables_gloo(world, n, p, lo_off):
+    N = n + p
+    _run(_zsolve_worker, world, n, p, lo_off, N - lo_off)
+
+
+def test_zsolve_tables_reject_thin_slabs():
+    import paper_2103_06998_b200 as adi
+
+    with pytest.raises(adi.AdiError) as e:  # N = 12, 4 ranks: 3 rows each < 2p = 4
+        adi.zsolve_tables(10, 2, 4, 0, 0, 12)
+    assert e.value.status == adi.ADI_ERR_ARG

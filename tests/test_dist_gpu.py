@@ -170,7 +170,8 @@ def test_box_mode_abi_contract():
 # The library's own distributed schedule (adi_step with nranks > 1) over the in-process
 # loopback transport: R host threads, one patch each, on cuda:0.
 # ---------------------------------------------------------------------------
-def run_loopback(R, n, p, tau, steps, mu_kind="uniform", source=False, eps_kind="phantom4", seed=17):
+def run_loopback(R, n, p, tau, steps, mu_kind="uniform", source=False, eps_kind="phantom4", seed=17, zsolve=0,
+                 active=None):
     import paper_2103_06998_b200 as adi
 
     N = n + p
@@ -193,6 +194,9 @@ def run_loopback(R, n, p, tau, steps, mu_kind="uniform", source=False, eps_kind=
     def work(r):
         try:
             P = adi.Patch(n, p, tau, device=0, rank=r, nranks=R, loopback=grp)
+            act = P.set_zsolve(zsolve)
+            if active is not None:
+                active[r] = act
             Nn, k0, k1 = P.layout()
             P.set_materials(eps, mu)
             P.set_fields([np.ascontiguousarray(x[k0:k1]).reshape(-1) for x in f])
@@ -227,6 +231,38 @@ def test_library_distributed_step_matches_oracle(R, n, p, mu_kind, source):
     for c in range(6):
         e = np.linalg.norm(got[c] - ref[c]) / np.linalg.norm(ref[c])
         assert e <= 1e-10, (c, e)
+
+
+@pytest.mark.parametrize("R,n,p,mu_kind,source", [(2, 10, 2, "uniform", True), (3, 22, 3, "uniform", False),
+                                                  (2, 12, 2, "random", False), (4, 30, 2, "uniform", True),
+                                                  (3, 13, 1, "uniform", False)])
+def test_library_partitioned_zsolve_matches_oracle(R, n, p, mu_kind, source):
+    """NEXT-1: the mass sweeps and derivative projections along the partitioned axis
+    solved in place by the SPIKE z-solve (tips, all-gather of 2p values per fiber, corrected segment
+    solve; no transposes for them) == the oracle's single-domain step (D16, <= 1e-10 per field), and
+    == the whole patch to 1e-12 (the partitioned solve reorders the rounding only)."""
+    tau, steps = 0.02, 3
+    act = [None] * R
+    got, eps, mu, f, _ = run_loopback(R, n, p, tau, steps, mu_kind, source, zsolve=1, active=act)
+    assert all(act), act
+    ref = oracle_ref(n, p, tau, steps, eps, mu, f, source)
+    whole = run_loopback(1, n, p, tau, steps, mu_kind, source)[0]
+    for c in range(6):
+        e = np.linalg.norm(got[c] - ref[c]) / np.linalg.norm(ref[c])
+        w = np.linalg.norm(got[c] - whole[c]) / np.linalg.norm(whole[c])
+        assert e <= 1e-10 and w <= 1e-12, (c, e, w)
+
+
+def test_partitioned_zsolve_falls_back_when_slabs_are_thin():
+    """A rank with fewer than 2p active rows cannot host the p-row interface blocks: mode 1 reports
+    inactive and the step keeps the transposes (still == the oracle)."""
+    act = [None] * 3
+    tau, steps = 0.02, 1
+    got, eps, mu, f, _ = run_loopback(3, 9, 3, tau, steps, zsolve=1, active=act)
+    assert not any(act)
+    ref = oracle_ref(9, 3, tau, steps, eps, mu, f)
+    for c in range(6):
+        assert np.linalg.norm(got[c] - ref[c]) <= 1e-10 * np.linalg.norm(ref[c])
 
 
 def test_library_distributed_bitwise_vs_whole_patch():

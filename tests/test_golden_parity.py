@@ -42,7 +42,7 @@ def _run_gpu(name):
 def test_golden_full_horizon(name):
     path = os.path.join(GOLD, f"{name}_golden.npz")
     if not os.path.exists(path):
-        pytest.fail(f"{path} missing: run tools/make_golden.py {name}")
+        pytest.fail(f"{path} missing: run tools/make_golden.py {name}")  # never skipped
     gd = np.load(path)
     I, out = _run_gpu(name)
     assert int(gd["steps"]) == I["steps"] and int(gd["n"]) == I["n"] and int(gd["p"]) == I["p"]

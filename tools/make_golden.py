@@ -70,21 +70,50 @@ def sample_indices(x: np.ndarray, seed: int) -> np.ndarray:
     return np.unique(np.concatenate([uni, top])).astype(np.int64)
 
 
-def main(name: str):
-    t0 = time.time()
-    I = inputs(name)
+CKPT = os.path.join(ROOT, "build", "golden_ckpt")
+CHUNK = 25
+
+
+def _patch(I, fields, m0):
+    """A fresh oracle patch holding ``fields`` after m0 steps: the source signal is shifted by m0
+    (the oracle reads signal[step_index], step_index counting from 0 on a fresh patch), so resuming
+    performs exactly the arithmetic of an uninterrupted run."""
     P = oracle.Patch(I["n"], I["p"], I["tau"])
     P.set_materials(I["eps"])
-    P.set_fields(I["fields"])
-    del I["fields"]
+    P.set_fields(fields)
     if I["source"] is not None:
         comp, pos, sig = I["source"]
         loads = [None, None, None]
         loads[comp] = P.point_load(*pos)
-        P.set_source(loads, sig)
+        P.set_source(loads, sig[m0:])
+    return P
+
+
+def main(name: str):
+    t0 = time.time()
+    I = inputs(name)
+    fields, m0, spent = I.pop("fields"), 0, 0.0
+    ck = os.path.join(CKPT, f"{name}.npz")
+    if os.path.exists(ck):  # resume a chunked run (checkpoints hold oracle output only)
+        d = np.load(ck)
+        fields, m0, spent = [d[f"f{c}"] for c in range(6)], int(d["m"]), float(d["spent"])
+        print(f"{name}: resuming after {m0} steps", flush=True)
+    P = _patch(I, fields, m0)
+    del fields
     t1 = time.time()
-    P.step(I["steps"])
+    m = m0
+    while m < I["steps"]:
+        k = min(CHUNK, I["steps"] - m) if I["steps"] > CHUNK else I["steps"] - m
+        P.step(k)
+        m += k
+        if m < I["steps"]:
+            os.makedirs(CKPT, exist_ok=True)
+            np.savez(ck + ".tmp.npz", m=m, spent=spent + time.time() - t1,
+                     **{f"f{c}": x for c, x in enumerate(P.get_fields())})
+            os.replace(ck + ".tmp.npz", ck)
+            print(f"{name}: {m}/{I['steps']} steps, {time.time() - t1:.0f} s", flush=True)
     t2 = time.time()
+    t2 += spent
     out = {"steps": I["steps"], "n": I["n"], "p": I["p"], "tau": I["tau"],
            "oracle_seconds": t2 - t1, "setup_seconds": t1 - t0}
     with open(os.path.join(ROOT, "oracle", "adi_oracle.c"), "rb") as f:
@@ -103,6 +132,8 @@ def main(name: str):
     path = os.path.join(GOLD, f"{name}_golden.npz")
     np.savez_compressed(path + ".tmp.npz", **out)
     os.replace(path + ".tmp.npz", path)
+    if os.path.exists(ck):
+        os.remove(ck)
     print(f"{name}: {I['steps']} steps in {t2 - t1:.1f} s (setup {t1 - t0:.1f} s); norms {norms}; wrote {path}",
           flush=True)
 
