@@ -237,6 +237,14 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
   const int u = tid & 15;
   const int xrow0 = tid >> 4;
   const bool iin = i < N;
+  // PEC activity (D1) of the thread's two output points, x / y part (the z part is per plane)
+  bool actxy[3][2];
+#pragma unroll
+  for (int d = 0; d < 3; d++)
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+      actxy[d][r] = i >= args.lo[d][0] && i < args.hi[d][0] && jA + r >= args.lo[d][1] && jA + r < args.hi[d][1] &&
+                    jA + r < N;
 
   // acc[g][jj][r]: output plane kin - P + jj of the current input plane kin (jj = 0: completes
   // now); after the output the window shifts by one plane (register moves, static indices)
@@ -253,13 +261,19 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
         double ld[3][2];
 #pragma unroll
         for (int r = 0; r < 2; r++) {
-          const int j = jA + r;
-          const bool ok = kout && j < N;
-          const int64_t I = ok ? i + (int64_t)N * j + NN * k : 0;
-          sc[r][0] = ok ? args.a[I] : 0.0;
-          sc[r][1] = ok ? args.c[I] : 0.0;
+          sc[r][0] = sc[r][1] = 0.0;
 #pragma unroll
-          for (int d = 0; d < 3; d++) ld[d][r] = (ok && sval != 0.0 && args.load[d]) ? args.load[d][I] : 0.0;
+          for (int d = 0; d < 3; d++) ld[d][r] = 0.0;
+          if (kout && jA + r < N) {
+            const int64_t I = i + (int64_t)N * (jA + r) + NN * k;
+            sc[r][0] = args.a[I];
+            sc[r][1] = args.c[I];
+            if (sval != 0.0) {
+#pragma unroll
+              for (int d = 0; d < 3; d++)
+                if (args.load[d]) ld[d][r] = args.load[d][I];
+            }
+          }
         }
         double* sx = sx0 + (NSX == 2 ? (it & 1) * (NXS * HY * RX_TX) : 0);
         mbar_wait(&bar[st], (unsigned)((it / RX_RING) & 1));
@@ -363,15 +377,14 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
           const int slotk = 0;
           if (kout) {
 #pragma unroll
-            for (int r = 0; r < 2; r++) {
-              const int j = jA + r;
-              if (j < N) {
+            for (int d = 0; d < 3; d++) {
+              const bool actz = kg0 + k >= args.lo[d][2] && kg0 + k < args.hi[d][2];
 #pragma unroll
-                for (int d = 0; d < 3; d++) {
-                  const bool act = i >= args.lo[d][0] && i < args.hi[d][0] && j >= args.lo[d][1] &&
-                                   j < args.hi[d][1] && kg0 + k >= args.lo[d][2] && kg0 + k < args.hi[d][2];
+              for (int r = 0; r < 2; r++) {
+                const int j = jA + r;
+                if (j < N) {
                   double val = 0.0;
-                  if (act) {
+                  if (actz && actxy[d][r]) {
                     val = acc[3 * d][slotk][r] + sc[r][0] * acc[3 * d + 1][slotk][r] + sc[r][1] * acc[3 * d + 2][slotk][r];
                     if (sval != 0.0) val -= sc[r][0] * sval * ld[d][r];
                   }
