@@ -59,6 +59,7 @@ def lib():
             L.orc_project_weighted.argtypes = [C.c_void_p, _dp, _dp, _dp]
             L.orc_point_load.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, _dp]
             L.orc_set_source.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_int64]
+            L.orc_set_rhs_variant.argtypes = [C.c_void_p, C.c_int]
             _lib = L
         return _lib
 
@@ -178,6 +179,11 @@ class Patch:
 
     def set_order_variant(self, v: int):
         self._L.orc_set_order_variant(self.h, int(v))
+
+    def set_rhs_variant(self, v: int):
+        """0: material of the test function on the RHS rows (D5); 2: element-wise material inside
+        the RHS quadrature (V2, NEXT-2; needs set_materials with element values)."""
+        self._L.orc_set_rhs_variant(self.h, int(v))
 
     @property
     def max_growth(self) -> float:

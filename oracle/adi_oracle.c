@@ -51,6 +51,9 @@ typedef struct {
   int64_t step_index;
   int have_fields;
   int order_variant; /* 0 = stiffened axis first (D7), 1 = paper-literal x->y->z (V1) */
+  int rhs_variant;   /* 0 = material of the test function on the RHS rows (D5); 2 = element-wise
+                        material inside the RHS quadrature (V2) */
+  double *eps_el, *mu_el; /* element-wise material of the last orc_set_materials (NULL after _tf) */
   double max_growth; /* max growth factor seen in banded LU (pin P9) */
 } orc_patch;
 
@@ -177,6 +180,7 @@ void orc_destroy(orc_patch* P) {
   for (int i = 0; i < 6; i++) free(P->F[i]);
   for (int i = 0; i < 3; i++) free(P->load[i]);
   free(P->signal);
+  free(P->eps_el); free(P->mu_el);
   free(P);
 }
 
@@ -299,10 +303,16 @@ int orc_set_materials(orc_patch* P, const double* eps_e, const double* mu_e) {
   free(w);
   (void)U;
   derive_abc(P);
+  free(P->eps_el); free(P->mu_el);
+  P->eps_el = (double*)malloc(sizeof(double) * ne);
+  P->mu_el = (double*)malloc(sizeof(double) * ne);
+  for (int64_t e = 0; e < ne; e++) { P->eps_el[e] = eps_e[e]; P->mu_el[e] = mu_e ? mu_e[e] : 1.0; }
   return ORC_OK;
 }
 
 int orc_set_materials_tf(orc_patch* P, const double* eps_tf, const double* mu_tf) {
+  free(P->eps_el); free(P->mu_el);
+  P->eps_el = P->mu_el = NULL; /* per-test-function input: no element-wise material (V2 unavailable) */
   int64_t U = (int64_t)P->N * P->N * P->N;
   if (!eps_tf) { set_err("orc_set_materials_tf: eps is NULL"); return ORC_ERR_ARG; }
   for (int64_t I = 0; I < U; I++) {
@@ -580,6 +590,121 @@ static double source_value(const orc_patch* P) {
  *   R2 = M^3 E2 + a.[...]               + c.(B(x)A(x)M) E1
  *   R3 = M^3 E3 + a.[...]               + c.(M(x)B(x)A) E2
  * minus a.s.J (D9); rows of PEC-eliminated test functions are zeroed (D1). */
+/* ---- NEXT-2 variant V2: element-wise material inside the RHS quadrature ---------------------
+ * Literal reading of "element-wise eps, mu" / "RHS-hat with material data": every
+ * material-carrying RHS term is the Galerkin integral with the element's coefficient inside,
+ *   [sum_e w_e (X^{e_x} (x) Y^{e_y} (x) Z^{e_z}) u]_{rst},
+ * X^{a} the element-a part of the 1D matrix X (Gauss q = p+1 on element a: M^a_{il} = int_a B_i B_l,
+ * A^a_{il} = int_a B_i B_l', B^a = (A^a)^T), summed element by element (no Kronecker factoring). */
+static void element_matrices(const orc_patch* P, double* Me, double* Ae) {
+  int n = P->n, p = P->p, N = P->N, q = p + 1, w1 = p + 1;
+  double gx[16], gw[16];
+  gauss_legendre(q, gx, gw);
+  double* v = (double*)malloc(sizeof(double) * N);
+  double* d = (double*)malloc(sizeof(double) * N);
+  memset(Me, 0, sizeof(double) * n * w1 * w1);
+  memset(Ae, 0, sizeof(double) * n * w1 * w1);
+  for (int e = 0; e < n; e++) {
+    double x0 = P->t[p + e], x1 = P->t[p + e + 1], h = x1 - x0;
+    for (int g = 0; g < q; g++) {
+      double x = x0 + 0.5 * h * (gx[g] + 1.0), w = 0.5 * h * gw[g];
+      basis_all(P->t, n, p, x, v, d);
+      for (int i = 0; i <= p; i++)
+        for (int l = 0; l <= p; l++) {
+          Me[(e * w1 + i) * w1 + l] += v[e + i] * v[e + l] * w;
+          Ae[(e * w1 + i) * w1 + l] += v[e + i] * d[e + l] * w;
+        }
+    }
+  }
+  free(v);
+  free(d);
+}
+
+/* op: 0 = M, 1 = A, 2 = B; entry (test i, trial l) of element e's local matrix */
+static double eloc(const double* Me, const double* Ae, int p, int op, int e, int i, int l) {
+  int w1 = p + 1;
+  if (op == 0) return Me[(e * w1 + i) * w1 + l];
+  if (op == 1) return Ae[(e * w1 + i) * w1 + l];
+  return Ae[(e * w1 + l) * w1 + i];
+}
+
+static void kron3_w(const orc_patch* P, const double* Me, const double* Ae, int ox, int oy, int oz,
+                    const double* w_el, const double* u, double* out) {
+  int n = P->n, p = P->p, N = P->N;
+  memset(out, 0, sizeof(double) * (int64_t)N * N * N);
+  for (int c = 0; c < n; c++)
+    for (int b = 0; b < n; b++)
+      for (int a = 0; a < n; a++) {
+        double we = w_el[a + (int64_t)n * (b + (int64_t)n * c)];
+        for (int k = 0; k <= p; k++)
+          for (int j = 0; j <= p; j++)
+            for (int i = 0; i <= p; i++) {
+              double acc = 0.0;
+              for (int o = 0; o <= p; o++)
+                for (int m = 0; m <= p; m++)
+                  for (int l = 0; l <= p; l++)
+                    acc += eloc(Me, Ae, p, ox, a, i, l) * eloc(Me, Ae, p, oy, b, j, m) *
+                           eloc(Me, Ae, p, oz, c, k, o) * u[IDX(N, a + l, b + m, c + o)];
+              out[IDX(N, a + i, b + j, c + k)] += we * acc;
+            }
+      }
+}
+
+void orc_set_rhs_variant(orc_patch* P, int v) { P->rhs_variant = v; }
+
+/* V2 right-hand sides of the E systems: the D5 terms of rhs_E below with a = tau/(2 eps_e) and
+ * c = tau^2/(4 eps_e mu_e) of each element inside the integrals; M^3 E carries no material; the
+ * source keeps the row factor of D9. */
+static void rhs_E_v2(orc_patch* P, int s, double* const* R) {
+  int n = P->n, p = P->p;
+  int64_t U = (int64_t)P->N * P->N * P->N, ne = (int64_t)n * n * n;
+  double* Me = (double*)malloc(sizeof(double) * n * (p + 1) * (p + 1));
+  double* Ae = (double*)malloc(sizeof(double) * n * (p + 1) * (p + 1));
+  element_matrices(P, Me, Ae);
+  double* ae = (double*)malloc(sizeof(double) * ne);
+  double* ce = (double*)malloc(sizeof(double) * ne);
+  for (int64_t e = 0; e < ne; e++) {
+    ae[e] = P->tau / (2.0 * P->eps_el[e]);
+    ce[e] = P->tau * P->tau / (4.0 * P->eps_el[e] * P->mu_el[e]);
+  }
+  double* t1 = (double*)malloc(sizeof(double) * U);
+  double* t2 = (double*)malloc(sizeof(double) * U);
+  double* t3 = (double*)malloc(sizeof(double) * U);
+  double* t4 = (double*)malloc(sizeof(double) * U);
+  double** E = P->F;
+  double** H = P->F + 3;
+  double sv = source_value(P);
+  for (int d = 0; d < 3; d++) {
+    kron3(P, P->M, 0, P->M, 0, P->M, 0, E[d], t1);
+    if (d == 0) {
+      kron3_w(P, Me, Ae, 0, 0, 1, ae, H[1], t2);
+      kron3_w(P, Me, Ae, 0, 1, 0, ae, H[2], t3);
+      for (int64_t I = 0; I < U; I++) t2[I] = -t2[I] + t3[I];
+      if (s == 1) kron3_w(P, Me, Ae, 1, 2, 0, ce, E[1], t4);
+      else        kron3_w(P, Me, Ae, 1, 0, 2, ce, E[2], t4);
+    } else if (d == 1) {
+      kron3_w(P, Me, Ae, 0, 0, 1, ae, H[0], t2);
+      kron3_w(P, Me, Ae, 1, 0, 0, ae, H[2], t3);
+      for (int64_t I = 0; I < U; I++) t2[I] = t2[I] - t3[I];
+      if (s == 1) kron3_w(P, Me, Ae, 0, 1, 2, ce, E[2], t4);
+      else        kron3_w(P, Me, Ae, 2, 1, 0, ce, E[0], t4);
+    } else {
+      kron3_w(P, Me, Ae, 0, 1, 0, ae, H[0], t2);
+      kron3_w(P, Me, Ae, 1, 0, 0, ae, H[1], t3);
+      for (int64_t I = 0; I < U; I++) t2[I] = -t2[I] + t3[I];
+      if (s == 1) kron3_w(P, Me, Ae, 2, 0, 1, ce, E[0], t4);
+      else        kron3_w(P, Me, Ae, 0, 2, 1, ce, E[1], t4);
+    }
+    for (int64_t I = 0; I < U; I++) {
+      double v = t1[I] + t2[I] + t4[I];
+      if (P->load[d]) v -= P->a[I] * sv * P->load[d][I];
+      R[d][I] = v;
+    }
+    zero_inactive(P, d, R[d]);
+  }
+  free(t1); free(t2); free(t3); free(t4); free(Me); free(Ae); free(ae); free(ce);
+}
+
 static void rhs_E(orc_patch* P, int s, double* const* R) {
   int64_t U = (int64_t)P->N * P->N * P->N;
   const double *M = P->M, *A = P->A;
@@ -668,7 +793,8 @@ static int substep(orc_patch* P, int s) {
     G[d] = (double*)malloc(sizeof(double) * U);
     memcpy(Eo[d], P->F[d], sizeof(double) * U);
   }
-  rhs_E(P, s, R);
+  if (P->rhs_variant == 2) rhs_E_v2(P, s, R);
+  else rhs_E(P, s, R);
   for (int d = 0; d < 3 && st == ORC_OK; d++) st = solve_E(P, s, d, R[d]);
   if (st == ORC_OK) {
     rhs_H(P, s, Eo, R, G);
@@ -685,6 +811,7 @@ static int substep(orc_patch* P, int s) {
 
 int orc_step(orc_patch* P, int64_t k) {
   if (!P->have_fields) { set_err("orc_step: fields not set"); return ORC_ERR_STATE; }
+  if (P->rhs_variant == 2 && !P->eps_el) { set_err("orc_step: V2 needs element-wise materials (orc_set_materials)"); return ORC_ERR_STATE; }
   if (k < 0) { set_err("orc_step: k < 0"); return ORC_ERR_ARG; }
   for (int64_t i = 0; i < k; i++) {
     int st;
@@ -698,7 +825,15 @@ int orc_step(orc_patch* P, int64_t k) {
 /* ---- debug entry points (per-stage parity / pins) ----------------------- */
 
 /* RHS of the E systems of substep s from the current fields (3 outputs). */
-int orc_debug_rhs_e(orc_patch* P, int s, double* const* R) { rhs_E(P, s, R); return ORC_OK; }
+int orc_debug_rhs_e(orc_patch* P, int s, double* const* R) {
+  if (P->rhs_variant == 2) {
+    if (!P->eps_el) { set_err("orc_debug_rhs_e: V2 needs element-wise materials"); return ORC_ERR_STATE; }
+    rhs_E_v2(P, s, R);
+  } else {
+    rhs_E(P, s, R);
+  }
+  return ORC_OK;
+}
 
 /* RHS of the H systems of substep s, given Eo (start of substep) and En. */
 int orc_debug_rhs_h(orc_patch* P, int s, double* const* Eo, double* const* En, double* const* G) {

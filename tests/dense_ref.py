@@ -42,9 +42,15 @@ class DenseMaxwell:
         self.D = [K(Bv, Bv, Bd), K(Bv, Bd, Bv), K(Bd, Bv, Bv)]  # d/dx1, d/dx2, d/dx3
         self.W = np.kron(np.kron(w, w), w)
 
+        # element of each 3D Gauss point (x fastest, q points per element per axis)
+        ex = np.repeat(np.arange(n), q)
+        self.elem_of_point = (ex[None, None, :] + n * (ex[None, :, None] + n * ex[:, None, None])).reshape(-1)
+
     # (f, g) with f = trial operator, g = test operator: rows = test functions
-    def form(self, test, trial):
-        return test.T @ (self.W[:, None] * trial)
+    def form(self, test, trial, weight=None):
+        """weight: optional coefficient at every 3D Gauss point (V2: the element's material)."""
+        W = self.W if weight is None else self.W * weight
+        return test.T @ (W[:, None] * trial)
 
     def active(self, comp: int) -> np.ndarray:
         """Boolean mask of active coefficients (D1)."""
@@ -59,12 +65,15 @@ class DenseMaxwell:
         # back to x-fastest flat order
         return m.transpose(2, 1, 0).reshape(-1)
 
-    def step(self, E, H, a, b, c, s_val=0.0, J=None):
+    def step(self, E, H, a, b, c, s_val=0.0, J=None, v2=None):
         """One full step (weak1 -> weak2 -> weak3 -> weak4).
 
         E, H: lists of 3 flat arrays; a, b, c: per-test-function row factors
         tau/(2 eps), tau/(2 mu), tau^2/(4 eps mu); J: list of 3 load vectors
         or None; s_val the signal value of this step (D9).
+        v2: None (D5) or element arrays (a_e, c_e) = (tau/(2 eps_e), tau^2/(4 eps_e mu_e)): variant V2,
+        the E right-hand sides' curl and mixed-derivative integrals with the element's coefficient
+        inside the 3D quadrature (no row factor on those terms); LHS, H systems and source unchanged.
         """
         Phi, D = self.Phi, self.D
         Mass = self.form(Phi, Phi)
@@ -72,6 +81,13 @@ class DenseMaxwell:
         Adv = [self.form(Phi, D[ax]) for ax in range(3)]
         # (d_a trial, d_b test)
         Mix = lambda ta, tb: self.form(D[tb], D[ta])
+        if v2 is None:
+            aAdv = [a[:, None] * X for X in Adv]
+            cMix = lambda ta, tb: c[:, None] * Mix(ta, tb)
+        else:
+            wa, wc = (np.asarray(x, dtype=float)[self.elem_of_point] for x in v2)
+            aAdv = [self.form(Phi, D[ax], wa) for ax in range(3)]
+            cMix = lambda ta, tb: self.form(D[tb], D[ta], wc)
         Stf = [Mix(ax, ax) for ax in range(3)]
         E = [np.asarray(e, dtype=float).copy() for e in E]
         H = [np.asarray(h, dtype=float).copy() for h in H]
@@ -95,9 +111,9 @@ class DenseMaxwell:
         # RHS: (E^n,V) + a[(-d3 H2 + d2 H3, V1) + (d3 H1 - d1 H3, V2) + (-d2 H1 + d1 H2, V3)]
         #      + c[(d1 E2, d2 V1) + (d2 E3, d3 V2) + (d3 E1, d1 V3)]
         R = [
-            Mass @ E[0] + a * (-Adv[2] @ H[1] + Adv[1] @ H[2]) + c * (Mix(0, 1) @ E[1]) + source(0),
-            Mass @ E[1] + a * (Adv[2] @ H[0] - Adv[0] @ H[2]) + c * (Mix(1, 2) @ E[2]) + source(1),
-            Mass @ E[2] + a * (-Adv[1] @ H[0] + Adv[0] @ H[1]) + c * (Mix(2, 0) @ E[0]) + source(2),
+            Mass @ E[0] + (-aAdv[2] @ H[1] + aAdv[1] @ H[2]) + cMix(0, 1) @ E[1] + source(0),
+            Mass @ E[1] + (aAdv[2] @ H[0] - aAdv[0] @ H[2]) + cMix(1, 2) @ E[2] + source(1),
+            Mass @ E[2] + (-aAdv[1] @ H[0] + aAdv[0] @ H[1]) + cMix(2, 0) @ E[0] + source(2),
         ]
         Eh = [solve_E(1, 0, R[0]), solve_E(2, 1, R[1]), solve_E(0, 2, R[2])]
         # ---- weak2: substep-1 H systems -------------------------
@@ -115,9 +131,9 @@ class DenseMaxwell:
         # LHS: (E1,V1)+c(d3 E1,d3 V1); (E2,V2)+c(d1 E2,d1 V2); (E3,V3)+c(d2 E3,d2 V3)
         # RHS: (E^h,V) + a[C-term with H^h] + c[(d1 E3,d3 V1)+(d2 E1,d1 V2)+(d3 E2,d2 V3)]
         R = [
-            Mass @ Eh[0] + a * (-Adv[2] @ Hh[1] + Adv[1] @ Hh[2]) + c * (Mix(0, 2) @ Eh[2]) + source(0),
-            Mass @ Eh[1] + a * (Adv[2] @ Hh[0] - Adv[0] @ Hh[2]) + c * (Mix(1, 0) @ Eh[0]) + source(1),
-            Mass @ Eh[2] + a * (-Adv[1] @ Hh[0] + Adv[0] @ Hh[1]) + c * (Mix(2, 1) @ Eh[1]) + source(2),
+            Mass @ Eh[0] + (-aAdv[2] @ Hh[1] + aAdv[1] @ Hh[2]) + cMix(0, 2) @ Eh[2] + source(0),
+            Mass @ Eh[1] + (aAdv[2] @ Hh[0] - aAdv[0] @ Hh[2]) + cMix(1, 0) @ Eh[0] + source(1),
+            Mass @ Eh[2] + (-aAdv[1] @ Hh[0] + aAdv[0] @ Hh[1]) + cMix(2, 1) @ Eh[1] + source(2),
         ]
         E1 = [solve_E(2, 0, R[0]), solve_E(0, 1, R[1]), solve_E(1, 2, R[2])]
         # ---- weak4: substep-2 H systems -------------------------

@@ -258,6 +258,81 @@ def test_P2_dense_natural_bc(p):
     assert _dense_vs_oracle(n, p, 0.1, "random", 2, seed=50 + p, source=True, bc=1) <= 1e-10
 
 
+def _v2_vs_dense(n, p, tau, steps, seed, source=False):
+    """Oracle V2 step (element-wise material inside the RHS quadrature) vs the dense weak-form
+    assembly with the element coefficient at every 3D Gauss point (tests/dense_ref.py)."""
+    N = n + p
+    U = N ** 3
+    rng = np.random.default_rng(seed)
+    eps_e = rng.uniform(1, 80, n ** 3)
+    mu_e = rng.uniform(0.5, 2.0, n ** 3)
+    fields = workloads.random_fields(N, seed)
+    P = oracle.Patch(n, p, tau)
+    P.set_materials(eps_e, mu_e)
+    P.set_rhs_variant(2)
+    eps_tf, mu_tf = P.get_materials_tf()
+    a, b, c = tau / (2 * eps_tf), tau / (2 * mu_tf), tau * tau / (4 * eps_tf * mu_tf)
+    J, sig = None, np.zeros(steps)
+    if source:
+        J = [None, rng.uniform(-1, 1, U), None]
+        sig = rng.uniform(-1, 1, steps)
+        P.set_source(J, sig)
+    P.set_fields(fields)
+    P.step(steps)
+    got = P.get_fields()
+    D = DenseMaxwell(n, p, tau)
+    E = [f.copy() for f in fields[:3]]
+    H = [f.copy() for f in fields[3:]]
+    v2 = (tau / (2 * eps_e), tau * tau / (4 * eps_e * mu_e))
+    for k in range(steps):
+        E, H = D.step(E, H, a, b, c, s_val=sig[k], J=J, v2=v2)
+    return max(rel(got[d], (E + H)[d]) for d in range(6)), got, (eps_e, mu_e, fields)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_V2_dense(p):
+    """NEXT-2 V2 (P:548-549 read as element-wise eps, mu inside the RHS integrals): the oracle's
+    element-by-element sums of local 1D matrices equal the dense 3D quadrature with the element's
+    coefficient at each Gauss point (no Kronecker factoring, scipy basis), 1 step; with p = 1 also
+    2 steps and a source."""
+    n = 3 if p == 3 else 4
+    err, _, _ = _v2_vs_dense(n, p, 0.05, 1, seed=70 + p)
+    assert err <= 1e-10, err
+    if p == 1:
+        err, _, _ = _v2_vs_dense(3, p, 0.1, 2, seed=77, source=True)
+        assert err <= 1e-10, err
+
+
+def test_V2_reduces_to_D5_for_constant_material_and_differs_otherwise():
+    """Uniform eps, mu: the element coefficient is the row factor, V2 == D5 (to rounding);
+    varying material: the two readings differ (the variant is not a no-op)."""
+    n, p, tau = 4, 2, 0.05
+    N = n + p
+    f = workloads.random_fields(N, 81)
+    out = {}
+    for mat in ("const", "random"):
+        eps_e = np.full(n ** 3, 7.5) if mat == "const" else np.random.default_rng(82).uniform(1, 80, n ** 3)
+        for v in (0, 2):
+            P = oracle.Patch(n, p, tau)
+            P.set_materials(eps_e)
+            P.set_rhs_variant(v)
+            P.set_fields(f)
+            P.step(2)
+            out[mat, v] = P.get_fields()
+    assert max(rel(out["const", 2][d], out["const", 0][d]) for d in range(6)) <= 1e-13
+    assert max(rel(out["random", 2][d], out["random", 0][d]) for d in range(3)) >= 1e-6
+
+
+def test_V2_needs_element_materials():
+    n, p = 3, 2
+    P = oracle.Patch(n, p, 0.05)
+    P.set_materials_tf(np.ones((n + p) ** 3))
+    P.set_rhs_variant(2)
+    P.set_fields(workloads.random_fields(n + p, 1))
+    with pytest.raises(Exception):
+        P.step(1)
+
+
 @pytest.mark.parametrize("p", [1, 2, 3])
 def test_point_load_vs_scipy(p):
     """orc_point_load (the oracle side of every c3/c4 source, D9): J_rst = B_r(x) B_s(y) B_t(z),
