@@ -159,6 +159,18 @@ adi_status adi_step(adi_patch patch, int64_t k);
  * ADI_ERR_ARG for other values. */
 adi_status adi_set_sweep_order(adi_patch patch, int32_t order);
 
+/* NEXT-2 variant V2: where the material enters the E right-hand sides.
+ *   0 (default, D5): every RHS row is scaled by its test function's a = tau/(2 eps^), c =
+ *      tau^2/(4 eps^ mu^) (P:545-549 read as "material data of the test B-spline");
+ *   2: "element-wise eps, mu" read literally -- the curl and mixed-derivative integrals of the E
+ *      right-hand sides carry each element's a_e, c_e INSIDE the Gauss quadrature (q = p + 1 per
+ *      element, sum-factorised interpolation / projection); the LHS (row-modified sweeps), the H
+ *      updates and the source keep the row factors.  Needs element materials (adi_set_materials;
+ *      after adi_set_materials_tf adi_step returns ADI_ERR_STATE) and allocates two (n (p+1))^3
+ *      work arrays (ADI_ERR_OOM if they do not fit).  Whole patches only (ADI_ERR_STATE otherwise).
+ * ADI_ERR_ARG for other values. */
+adi_status adi_set_rhs_variant(adi_patch patch, int32_t variant);
+
 /* NEXT-1 (the linear cost of banded direction solves): how a
  * distributed patch solves its CONSTANT sweeps along the partitioned axis z (the mass sweeps of
  * the E solves, a2/a6, and the M^{-1} of the uniform-mu derivative projections, a3/a4, a7/a8):

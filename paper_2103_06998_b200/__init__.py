@@ -41,6 +41,7 @@ EXPORTS = [
     "adi_box_sweep", "adi_box_factor", "adi_box_rhs", "adi_box_copy", "adi_box_abc", "adi_box_pec",
     "adi_box_materials_tf", "adi_set_sweep_order", "adi_energy", "adi_project_weighted", "adi_errors_uA", "adi_divergence",
     "adi_nccl_unique_id", "adi_loopback_create", "adi_loopback_destroy", "adi_set_zsolve", "adi_zsolve_tables",
+    "adi_set_rhs_variant",
 ]
 
 
@@ -157,6 +158,7 @@ def lib():
             L.adi_loopback_destroy.argtypes = [C.c_void_p]
             L.adi_loopback_destroy.restype = None
             L.adi_set_zsolve.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
+            L.adi_set_rhs_variant.argtypes = [C.c_void_p, C.c_int32]
             L.adi_zsolve_tables.argtypes = [C.c_int32] * 6 + [C.POINTER(C.c_int32)] * 2 + [C.c_void_p] * 4
             _lib = L
         return _lib
@@ -354,6 +356,11 @@ class Patch:
     def set_sweep_order(self, order: int):
         """0: stiffened axis first (D7, default); 1: paper-literal x -> y -> z (V1)."""
         self._check(self._L.adi_set_sweep_order(self.h, int(order)))
+
+    def set_rhs_variant(self, variant: int):
+        """NEXT-2: 0 = row factors of the test function on the E right-hand sides (D5, default);
+        2 = element-wise material inside their quadrature (V2)."""
+        self._check(self._L.adi_set_rhs_variant(self.h, int(variant)))
 
     def set_zsolve(self, mode: int) -> bool:
         """NEXT-1: 1 (default) partitioned (SPIKE) z-solve of the constant sweeps of a distributed

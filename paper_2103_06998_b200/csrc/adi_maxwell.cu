@@ -27,6 +27,7 @@
 #include "../../include/adi_maxwell.h"
 #include "dispatch.h"
 #include "setup_kernels.cuh"
+#include "rhs_v2.cuh"
 
 namespace {
 
@@ -244,6 +245,15 @@ struct adi_patch_s {
   size_t zsp_off[2][4] = {};
   double* ztips = nullptr;  // [3][2p][N^2]
   double* zgath = nullptr;  // [R][3][2p][N^2]
+  // NEXT-2 variant V2 (rhs_v2.cuh): element-wise material inside the E right-hand sides' quadrature
+  int rhs_variant = 0;                        // 0: D5 (row factors); 2: V2 (whole patch only)
+  double *el_eps = nullptr, *el_mu = nullptr;  // element material of the last adi_set_materials
+  bool have_el = false;
+  double* v2buf[2] = {nullptr, nullptr};      // Gauss-point work arrays, (n (p+1))^3 each
+  double* d_v2tab = nullptr;                  // interp value / derivative, projection value / derivative, M band
+  int* d_v2start = nullptr;                   // first input index of every row of those tables
+  size_t v2off[5] = {};
+  int v2soff[3] = {}, v2w[3] = {};            // starts offsets / widths: interpolation, projection, M
 };
 
 // Exchanges of the distributed (slab) mode; implementations below (NCCL, in-process loopback)
@@ -819,6 +829,122 @@ adi_status h_update_uniform_mu(adi_patch P, int s, const double* const H[3], con
   return st ? st : h_update_second(P, s, En, G);
 }
 
+// ---- NEXT-2 variant V2 (rhs_v2.cuh) ---------------------------------------------------------
+// Tables: interpolation to the q = p + 1 Gauss points of every element (value / derivative of the
+// p + 1 functions of the element), projection onto the test functions (value / derivative times
+// h w_g over the elements of the function's support), and the band of M (the M^3 E term).
+adi_status v2_setup(adi_patch P) {
+  if (P->d_v2tab) return ADI_OK;
+  const int n = P->n, p = P->p, N = P->N, q = p + 1, nq = n * q;
+  const int wi = p + 1, we = std::min(p + 1, n), wp = we * q, wm = std::min(2 * p + 1, N);
+  std::vector<double> gx, gw;
+  gauss01(q, gx, gw);
+  Space1D sp(n, p);
+  std::vector<double> IV((size_t)nq * wi), ID((size_t)nq * wi), PV((size_t)N * wp, 0.0), PD((size_t)N * wp, 0.0),
+      Mt((size_t)N * wm);
+  std::vector<int> st;
+  std::vector<double> v(p + 1), d(p + 1);
+  for (int e = 0; e < n; e++) {
+    const double a = sp.t[p + e], h = sp.t[p + e + 1] - a;
+    for (int g = 0; g < q; g++) {
+      sp.eval(a + h * gx[g], p + e, v.data(), d.data());
+      for (int l = 0; l <= p; l++) IV[(size_t)(e * q + g) * wi + l] = v[l], ID[(size_t)(e * q + g) * wi + l] = d[l];
+    }
+  }
+  for (int i = 0; i < nq; i++) st.push_back(i / q);
+  for (int r = 0; r < N; r++) {
+    const int se = std::min(std::max(r - p, 0), n - we);
+    st.push_back(se * q);
+    for (int t = 0; t < wp; t++) {
+      const int e = se + t / q, g = t % q, l = r - e;
+      if (l < 0 || l > p) continue;
+      const double a = sp.t[p + e], h = sp.t[p + e + 1] - a;
+      sp.eval(a + h * gx[g], p + e, v.data(), d.data());
+      PV[(size_t)r * wp + t] = h * gw[g] * v[l];
+      PD[(size_t)r * wp + t] = h * gw[g] * d[l];
+    }
+  }
+  for (int r = 0; r < N; r++) {
+    const int s0 = std::min(std::max(r - p, 0), N - wm);
+    st.push_back(s0);
+    for (int t = 0; t < wm; t++) Mt[(size_t)r * wm + t] = P->M[(size_t)r * N + s0 + t];
+  }
+  std::vector<double> all;
+  size_t k = 0;
+  for (auto* X : {&IV, &ID, &PV, &PD, &Mt}) P->v2off[k++] = all.size(), all.insert(all.end(), X->begin(), X->end());
+  P->v2soff[0] = 0, P->v2soff[1] = nq, P->v2soff[2] = nq + N;
+  P->v2w[0] = wi, P->v2w[1] = wp, P->v2w[2] = wm;
+  const size_t big = (size_t)nq * nq * nq;
+  if (cudaMalloc(&P->d_v2tab, all.size() * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&P->d_v2start, st.size() * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&P->v2buf[0], std::max(big, (size_t)P->U) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&P->v2buf[1], std::max(big, (size_t)P->U) * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    for (void* x : {(void*)P->d_v2tab, (void*)P->d_v2start, (void*)P->v2buf[0], (void*)P->v2buf[1]}) cudaFree(x);
+    P->d_v2tab = nullptr, P->d_v2start = nullptr, P->v2buf[0] = P->v2buf[1] = nullptr;
+    return fail(ADI_ERR_OOM, "V2: cudaMalloc of the Gauss-point work arrays (2 x %zu doubles)", big);
+  }
+  CUDA_TRY(cudaMemcpy(P->d_v2tab, all.data(), all.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(P->d_v2start, st.data(), st.size() * sizeof(int), cudaMemcpyHostToDevice));
+  return ADI_OK;
+}
+
+// E right-hand sides of substep s under V2 (same terms, signs and Kronecker placements as rhs3.cuh /
+// the oracle's rhs_E, D2-D4): R_d = M^3 E_d + sum_e a_e (curl terms)_e + sum_e c_e (mixed term)_e
+// - a s J_d (D9), PEC rows zeroed (D1).  Operators per axis: 0 = M, 1 = A (trial derivative),
+// 2 = B (test derivative).
+adi_status rhs_e_v2(adi_patch P, int s, const double* const F[6], double* const out[3]) {
+  if (!P->have_el) return fail(ADI_ERR_STATE, "V2 needs element-wise materials (adi_set_materials)");
+  adi_status st = v2_setup(P);
+  if (st) return st;
+  const int n = P->n, N = P->N, q = P->p + 1, nq = n * q;
+  const double* T = P->d_v2tab;
+  const int* S0 = P->d_v2start;
+  LaunchScope ls(P, ADI_K_RHS_E);
+  auto pass = [&](const double* in, int64_t d0, int64_t d1, int64_t d2, int ax, double* o, int64_t nout, int kind,
+                  bool der, double scale, int accumulate) {
+    // kind 0: interpolation (N -> nq), 1: projection (nq -> N), 2: M band (N -> N)
+    const double* tab = T + (kind == 0 ? P->v2off[der ? 1 : 0] : kind == 1 ? P->v2off[der ? 3 : 2] : P->v2off[4]);
+    adi::v2_pass_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(in, d0, d1, d2, ax, o, nout, tab, S0 + P->v2soff[kind],
+                                                           P->v2w[kind], scale, accumulate);
+  };
+  double *A = P->v2buf[0], *B = P->v2buf[1];
+  struct Term { int f, o[3], kind; double sign; };  // kind 0: a_e, 1: c_e
+  for (int d = 0; d < 3; d++) {
+    Term tm[3];
+    if (d == 0) {
+      tm[0] = {4, {0, 0, 1}, 0, -1.0}, tm[1] = {5, {0, 1, 0}, 0, 1.0};
+      tm[2] = s == 1 ? Term{1, {1, 2, 0}, 1, 1.0} : Term{2, {1, 0, 2}, 1, 1.0};
+    } else if (d == 1) {
+      tm[0] = {3, {0, 0, 1}, 0, 1.0}, tm[1] = {5, {1, 0, 0}, 0, -1.0};
+      tm[2] = s == 1 ? Term{2, {0, 1, 2}, 1, 1.0} : Term{0, {2, 1, 0}, 1, 1.0};
+    } else {
+      tm[0] = {3, {0, 1, 0}, 0, -1.0}, tm[1] = {4, {1, 0, 0}, 0, 1.0};
+      tm[2] = s == 1 ? Term{0, {2, 0, 1}, 1, 1.0} : Term{1, {0, 2, 1}, 1, 1.0};
+    }
+    pass(F[d], N, N, N, 0, A, N, 2, false, 1.0, 0);  // M^3 E_d
+    pass(A, N, N, N, 1, B, N, 2, false, 1.0, 0);
+    pass(B, N, N, N, 2, out[d], N, 2, false, 1.0, 0);
+    for (const Term& t : tm) {
+      pass(F[t.f], N, N, N, 0, A, nq, 0, t.o[0] == 1, 1.0, 0);
+      pass(A, nq, N, N, 1, B, nq, 0, t.o[1] == 1, 1.0, 0);
+      pass(B, nq, nq, N, 2, A, nq, 0, t.o[2] == 1, 1.0, 0);
+      adi::v2_weight_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(A, n, q, P->el_eps, P->el_mu, P->tau, t.kind);
+      pass(A, nq, nq, nq, 0, B, N, 1, t.o[0] == 2, 1.0, 0);
+      pass(B, N, nq, nq, 1, A, N, 1, t.o[1] == 2, 1.0, 0);
+      pass(A, N, N, nq, 2, out[d], N, 1, t.o[2] == 2, t.sign, 1);
+    }
+    if (P->load[d] && P->signal)
+      adi::v2_source_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(out[d], P->a, P->load[d], P->signal, P->d_step,
+                                                                P->nsig, P->U);
+    int lo[3], hi[3];
+    for (int ax = 0; ax < 3; ax++) active_range(P, d, ax, lo[ax], hi[ax]);
+    adi::pec_zero_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(out[d], N, lo[0], hi[0], lo[1], hi[1], lo[2], hi[2]);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
 adi_status substep(adi_patch P, int s) {
   adi_status st;
   const double* E[3] = {P->F[0], P->F[1], P->F[2]};
@@ -833,7 +959,9 @@ adi_status substep(adi_patch P, int s) {
     if ((st = h_update_first(P, s, H, E, P->G, P->stream2, P->ckpt2))) return st;
     CUDA_TRY(cudaEventRecord(P->ev_join, P->stream2));
   }
-  {
+  if (P->rhs_variant == 2) {
+    if ((st = rhs_e_v2(P, s, P->F, P->R))) return st;
+  } else {
     adi_status st3 = ADI_OK;
     if (rhs_e3(P, s, P->F, P->R, 0, 0, 0, 0, st3)) {
       if (st3) return st3;
@@ -1837,6 +1965,7 @@ void adi_destroy(adi_patch P) {
   for (int i = 0; i < 6; i++) f(P->Y[i]);
   f(P->cy), f(P->xbuf[0]), f(P->xbuf[1]);
   f(P->d_zsp[0]), f(P->d_zsp[1]), f(P->ztips), f(P->zgath);
+  f(P->el_eps), f(P->el_mu), f(P->v2buf[0]), f(P->v2buf[1]), f(P->d_v2tab), f(P->d_v2start);
   if (P->tr) {
     if (auto* L = dynamic_cast<LoopTransport*>(P->tr)) {
       std::lock_guard<std::mutex> lk(L->g->m);
@@ -2205,7 +2334,9 @@ adi_status adi_set_materials_tf(adi_patch P, const double* eps_tf, const double*
     cudaFree(m);
     return poison(P, st);
   }
-  return poison(P, set_tf(P, e, m));
+  st = set_tf(P, e, m);
+  if (!st) P->have_el = false;  // per-test-function input: V2 has no element material
+  return poison(P, st);
 }
 
 // element-wise -> per-test-function (D6): three separable passes on the GPU
@@ -2251,14 +2382,31 @@ adi_status adi_set_materials(adi_patch P, const double* eps_elem, const double* 
     }
   }
   cudaStreamSynchronize(P->stream);
-  cudaFree(de);
   cudaFree(dw);
   if (st) {
+    cudaFree(de);
     cudaFree(e);
     cudaFree(m);
     return poison(P, st);
   }
-  return poison(P, set_tf(P, e, m));
+  st = set_tf(P, e, m);
+  // NEXT-2 V2 keeps the element-wise material (whole patch): eps copied again, mu (or 1)
+  if (!st && !P->slab) {
+    if ((!P->el_eps && cudaMalloc(&P->el_eps, ne * sizeof(double)) != cudaSuccess) ||
+        (!P->el_mu && cudaMalloc(&P->el_mu, ne * sizeof(double)) != cudaSuccess)) {
+      cudaGetLastError();
+      st = fail(ADI_ERR_OOM, "adi_set_materials: element material arrays");
+    }
+    if (!st) st = copy_in(P, P->el_eps, eps_elem, ne);
+    if (!st) {
+      if (mu_elem) st = copy_in(P, P->el_mu, mu_elem, ne);
+      else adi::fill_kernel<<<P->nsm * 8, 256, 0, P->stream>>>(P->el_mu, ne, 1.0);
+    }
+    P->have_el = !st;
+  }
+  cudaStreamSynchronize(P->stream);
+  cudaFree(de);
+  return poison(P, st);
 }
 
 adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
@@ -2380,6 +2528,8 @@ adi_status adi_step(adi_patch P, int64_t k) {
     return fail(ADI_ERR_STATE, "box-mode patch (nranks > 1, no transport): use the adi_box_* entry points");
   if (k < 0) return fail(ADI_ERR_ARG, "adi_step: k < 0");
   if (!P->have_fields) return fail(ADI_ERR_STATE, "adi_step: fields not set");
+  if (P->rhs_variant == 2 && !P->have_el)
+    return fail(ADI_ERR_STATE, "adi_step: variant V2 needs element-wise materials (adi_set_materials)");
   if (k == 0) return ADI_OK;
   adi_status st = ADI_OK;
   if (P->timing || (P->slab && !P->tr->capturable())) {
@@ -2535,7 +2685,8 @@ adi_status adi_debug_rhs_e(adi_patch P, int32_t s, double* const R[3]) {
   const double* E[3] = {P->F[0], P->F[1], P->F[2]};
   const double* H[3] = {P->F[3], P->F[4], P->F[5]};
   adi_status st3 = ADI_OK;
-  if (rhs_e3(P, s, P->F, t, 0, 0, 0, 0, st3)) st = st3;  // the fused kernel where the step uses it
+  if (P->rhs_variant == 2) st = rhs_e_v2(P, s, P->F, t);
+  else if (rhs_e3(P, s, P->F, t, 0, 0, 0, 0, st3)) st = st3;  // the fused kernel where the step uses it
   else
     for (int d = 0; d < 3 && !st; d++) st = rhs_e(P, s, d, E, H, t[d]);
   for (int d = 0; d < 3 && !st; d++)
@@ -2708,6 +2859,19 @@ adi_status adi_set_sweep_order(adi_patch P, int32_t order) {
   if (order != 0 && order != 1) return fail(ADI_ERR_ARG, "adi_set_sweep_order: order %d not 0 or 1", order);
   drop_graph(P);
   P->sweep_order = order;
+  return ADI_OK;
+}
+
+adi_status adi_set_rhs_variant(adi_patch P, int32_t variant) {
+  CHECK_PATCH(P);
+  if (variant != 0 && variant != 2) return fail(ADI_ERR_ARG, "adi_set_rhs_variant: variant %d not 0 or 2", variant);
+  if (variant == 2 && P->cfg.nranks != 1) return fail(ADI_ERR_STATE, "adi_set_rhs_variant: V2 is whole-patch only");
+  if (variant == 2) {
+    adi_status st = v2_setup(P);
+    if (st) return st;
+  }
+  drop_graph(P);
+  P->rhs_variant = variant;
   return ADI_OK;
 }
 

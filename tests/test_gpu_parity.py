@@ -630,3 +630,70 @@ def test_fused_rhs_full_steps(fused):
         for n, p in [(34, 2), (64, 2), (33, 3)]:
             errs, _ = _parity_run(n, p, 0.01, 3, material="phantom4", source="modsine")
             assert max(errs) <= TOL_STEP, (n, p, errs)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2 variant V2: element-wise material inside the E right-hand sides' quadrature
+# (rhs_v2.cuh) against the oracle's element-by-element V2 (pinned by tests/test_oracle_pins.py
+# test_V2_dense against the dense 3D weak-form quadrature).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,p,s", [(4, 1, 1), (7, 2, 1), (7, 2, 2), (5, 3, 2), (12, 2, 1), (3, 4, 1)])
+def test_rhs_e_v2(n, p, s):
+    O, G = both(n, p, 0.05)
+    N = n + p
+    rng = np.random.default_rng(90 + n + p)
+    eps = rng.uniform(1, 80, n ** 3)
+    mu = rng.uniform(0.5, 2.0, n ** 3)
+    for X in (O, G):
+        X.set_materials(eps, mu)
+        X.set_rhs_variant(2)
+    f = workloads.random_fields(N, 91)
+    O.set_fields(f)
+    G.set_fields(f)
+    Ro, Rg = O.rhs_e(s), G.rhs_e(s)
+    for d in range(3):
+        assert rel(Rg[d], Ro[d]) <= 1e-13, (d, rel(Rg[d], Ro[d]))
+
+
+@pytest.mark.parametrize("n,p,material,source", [(8, 2, "phantom5", "pulse"), (9, 3, "phantom3", None),
+                                                 (14, 2, "phantom4", "modsine")])
+def test_v2_full_steps(n, p, material, source):
+    """V2 steps (E RHS by Gauss-point passes, everything else the production kernels) == the
+    oracle's V2 within D16's 1e-10; and V2 differs from D5 on the phantom (the variant matters)."""
+    tau, steps = 0.02, 3
+    O, G = both(n, p, tau)
+    N = n + p
+    eps = workloads.element_eps(n, material)
+    f = workloads.random_fields(N, 92)
+    for X in (O, G):
+        X.set_materials(eps)
+        X.set_rhs_variant(2)
+    O.set_fields(f)
+    G.set_fields(f)
+    if source is not None:
+        sig = workloads.signal(source, tau, steps)
+        pos = workloads.dipole_position(n)
+        O.set_source([None, None, O.point_load(*pos)], sig)
+        G.set_point_source(2, pos, sig)
+    O.step(steps)
+    G.step(steps)
+    fo, fg = O.get_fields(), G.get_fields()
+    assert max(rel(fg[c], fo[c]) for c in range(6)) <= TOL_STEP
+    G.set_rhs_variant(0)
+    G.set_fields(f)
+    G.step(steps)
+    assert max(rel(G.get_fields()[c], fo[c]) for c in range(3)) >= 1e-8
+
+
+def test_v2_contract():
+    n, p = 4, 2
+    G = adi.Patch(n, p, 0.05)
+    with pytest.raises(adi.AdiError) as e:
+        G.set_rhs_variant(1)
+    assert e.value.status == adi.ADI_ERR_ARG
+    G.set_materials_tf(np.ones((n + p) ** 3))
+    G.set_rhs_variant(2)
+    G.set_fields(workloads.random_fields(n + p, 1))
+    with pytest.raises(adi.AdiError) as e:  # per-test-function materials: no element material
+        G.step(1)
+    assert e.value.status == adi.ADI_ERR_STATE
