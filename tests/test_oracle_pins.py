@@ -604,6 +604,44 @@ def test_P5_spectral_radius(n, p, tau):
     assert rho <= 1 + 1e-12, rho
 
 
+def _amplification_el(n, p, tau, eps_e, variant):
+    """Amplification matrix of one oracle step with ELEMENT materials and the given RHS variant."""
+    P = oracle.Patch(n, p, tau)
+    P.set_materials(eps_e)
+    P.set_rhs_variant(variant)
+    N, U = P.N, P.N ** 3
+    masks = _masks(N)
+    idx = [(c, i) for c in range(6) for i in np.nonzero(masks[c])[0]]
+    G = np.zeros((len(idx), len(idx)))
+    for col, (c, i) in enumerate(idx):
+        f = [np.zeros(U) for _ in range(6)]
+        f[c][i] = 1.0
+        P.set_fields(f)
+        P.step(1)
+        out = P.get_fields()
+        G[:, col] = np.concatenate([out[cc][masks[cc]] for cc in range(6)])
+    return G
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_V2_is_unstable_where_D5_is_not(p):
+    """NEXT-2 finding (recorded in DESIGN.md): with a two-valued element material (eps 1 / 50, the
+    phantom's contrast) the paper-literal D5 step keeps rho(G) at 1 (p = 1; 1 + 1.3e-4 for p = 2,
+    the P5(iii) growth of the row-scaled scheme), while V2 -- the
+    element material inside the RHS quadrature but the test function's c^ in the row-modified
+    LHS, as the ADI solve requires -- has rho(G) > 1: the RHS mixed-derivative term no longer
+    matches the implicit stiffness it was eliminated against.  On the GPU the c3 / c4 phantoms
+    blow up under V2 within 40 steps (tools/v2_study.py)."""
+    n, tau = 3, 0.1
+    eps = np.where(np.random.default_rng(5).uniform(size=n ** 3) < 0.5, 1.0, 50.0)
+    rho5 = np.abs(np.linalg.eigvals(_amplification_el(n, p, tau, eps, 0))).max()
+    rho2 = np.abs(np.linalg.eigvals(_amplification_el(n, p, tau, eps, 2))).max()
+    # D5 with varying material: rho = 1 to rounding for p = 1; p = 2 shows the small growth of the
+    # row-scaled (non-normal) scheme recorded under P5(iii) (1.3e-4 here); V2 grows > 100x faster
+    assert rho5 - 1 <= (1e-12 if p == 1 else 1e-3), rho5
+    assert rho2 - 1 >= max(0.01, 100 * (rho5 - 1)), (rho2, rho5)
+
+
 def _mass_sqrt(n, p):
     D = DenseMaxwell(n, p, 1.0)
     masks, _, Mb, _, _ = D.pr_operators(np.zeros(D.U), np.zeros(D.U))
