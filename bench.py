@@ -49,7 +49,7 @@ def dof_count(n: int, p: int) -> int:
     return 3 * N * (N - 2) ** 2 + 3 * N ** 3
 
 
-def step_class_bytes(n: int, p: int, mu_uniform: bool = True):
+def step_class_bytes(n: int, p: int, mu_uniform: bool = True, fused_h: bool = True):
     """Algorithmic HBM bytes of one time step per kernel class, in SURVEY.md §8(a)/§8(d)'s
     counting (compulsory traffic of each hot-path step, independent of how many launches the
     schedule spends on it).  U = N^3 stored coefficients; Ue = N (N-2)^2 active rows of an E
@@ -58,7 +58,11 @@ def step_class_bytes(n: int, p: int, mu_uniform: bool = True):
       sweep_mod  (a2/a6 first sweep): 24 B per active row (read f, c; write x), 3 components -> 9 Ue
       sweep_mass (a2/a6 other two sweeps): 16 B per active row, 2 x 3 components       -> 12 Ue
       sweep_der  (a3+a4 / a7+a8, uniform mu: the exact derivative-projection identity of
-                  SURVEY §8(a)'s note): 24 B per row (read u, base; write out), 2 x 3 -> 18 U
+                  SURVEY §8(a)'s note): 24 B per row (read u, base; write out), 2 x 3 -> 18 U;
+                  fused schedule (fused_h, the library's default for whole patches): the second
+                  projection of a substep and the first of the next apply the same operator to
+                  the same field, one pass writes both (read u, Q; write H, Q'): 32 B per row,
+                  3 components -> 12 U
       rhs_h      (general mu only, a3/a7): read H_d, Eo, En, b; write G_d, 3 components -> 15 U
                   (then 9 mass sweeps over H: 18 U, counted under sweep_mass)
     Uniform mu: 29 U + 21 Ue words per substep, i.e. (58 U + 42 Ue) * 8 B per step."""
@@ -68,16 +72,17 @@ def step_class_bytes(n: int, p: int, mu_uniform: bool = True):
     w = 8.0
     out = {"rhs_e": 2 * 11 * U * w, "sweep_mod": 2 * 9 * Ue * w, "sweep_mass": 2 * 12 * Ue * w}
     if mu_uniform:
-        out["sweep_der"] = 2 * 18 * U * w
+        out["sweep_der"] = 2 * (12 if fused_h else 18) * U * w
     else:
         out["rhs_h"] = 2 * 15 * U * w
         out["sweep_mass"] += 2 * 18 * U * w
     return out
 
 
-def step_bytes(n: int, p: int) -> float:
-    """Compulsory HBM bytes of one step of the schedule run (uniform mu): (58 U + 42 Ue) * 8 B."""
-    return sum(step_class_bytes(n, p).values())
+def step_bytes(n: int, p: int, fused_h: bool = True) -> float:
+    """Compulsory HBM bytes of one step of the schedule run (uniform mu): (58 U + 42 Ue) * 8 B, or
+    (46 U + 42 Ue) * 8 B with the fused H projections."""
+    return sum(step_class_bytes(n, p, fused_h=fused_h).values())
 
 
 def hbm_peak():
@@ -292,8 +297,9 @@ def parallelism_label(args):
     if ws == 1:
         return "single GPU, whole patch, CUDA graph per step"
     return (f"z-slab decomposition over {ws} GPUs (one process per GPU), the library's distributed adi_step: "
-            "NCCL halo exchange before the RHS stencils, batched all-to-all z<->y transposes around the z sweeps, "
-            "one CUDA graph per step")
+            "NCCL halo exchange before the RHS stencils; mass sweeps and derivative projections along z by the "
+            "partitioned (SPIKE) solve in place (2p interface values per fiber all-gathered, NEXT-1); batched "
+            "all-to-all z<->y transposes only around the row-modified z sweep; one CUDA graph per step")
 
 
 def config_dict(cfg, args):
@@ -345,7 +351,8 @@ class _Whole:
 
 class _Dist:
     """N > 1 GPUs: this rank's z-slab patch; the library runs the distributed schedule itself
-    (adi_step over NCCL: halo exchanges and batched z<->y transposes, one CUDA graph per step)."""
+    (adi_step over NCCL: halo exchanges, the partitioned z-solve of the constant sweeps, batched
+    z<->y transposes around the row-modified z sweep; one CUDA graph per step)."""
 
     def __init__(self, cfg, local, seed):
         import torch
@@ -355,6 +362,7 @@ class _Dist:
         n, p, tau = cfg["n"], cfg["p"], cfg["tau"]
         self.N = N = n + p
         self.G = create_patch(n, p, tau, device=local)
+        self.zsolve_active = self.G.set_zsolve(1)
         _, k0, k1 = self.G.layout()
         self.nz = k1 - k0
         self.G.set_materials(workloads.element_eps(n, cfg["material"]))
@@ -450,7 +458,7 @@ def run_ours(args, cfg):
     # roofline of the dominant kernel class: survey bytes of the class per step, divided over
     # the class's launches per step (rep covers `timed_steps` steps)
     peak, peak_src = hbm_peak()
-    cls_bytes = step_class_bytes(n, p)
+    cls_bytes = step_class_bytes(n, p, fused_h=(ws == 1))  # the slab path keeps two projections
     algo = {k: v * S.timed_steps / rep[k][1] for k, v in cls_bytes.items() if rep.get(k, (0, 0))[1] > 0}
     cls = max(algo, key=lambda k: rep[k][0])
     t_cls, n_cls = rep[cls]
@@ -476,7 +484,7 @@ def run_ours(args, cfg):
             kd["frac"] = kd["achieved_gbs"] / peak
         kernels[k] = kd
     # end-to-end HBM fraction of the step (algorithmic bytes of the schedule run)
-    sbytes = step_bytes(n, p)
+    sbytes = step_bytes(n, p, fused_h=(ws == 1))
     cpu = None
     if not args.no_cpu_baseline and ws == 1:  # the CPU oracle baseline: rank 0 at N = 1 only
         rate, dt, desc, extra = cpu_oracle_rate(cfg, args.oracle_steps, args.oracle_n)

@@ -245,6 +245,15 @@ struct adi_patch_s {
   size_t zsp_off[2][4] = {};
   double* ztips = nullptr;  // [3][2p][N^2]
   double* zgath = nullptr;  // [R][3][2p][N^2]
+  // Fused H projections (uniform mu, whole patch): the second derivative projection of a substep
+  // and the first one of the next substep apply the SAME operator to the SAME new E component
+  // (axis a2(s) = a1(s+1), field x2(s) = x1(s+1), coefficient c2(s) = c1(s+1), both substeps and
+  // across the step boundary), so one launch writes both: H_new = Q + c x and Q' = H_new + c x.
+  // Q (the next substep's partially updated H) persists between steps; q_valid = false after any
+  // change of fields / tau / materials: adi_step then runs the first projection once, eagerly.
+  double* Q[3] = {nullptr, nullptr, nullptr};
+  bool q_valid = false;
+  int hmerge = 1;  // ADI_HMERGE=0 disables
   // NEXT-2 variant V2 (rhs_v2.cuh): element-wise material inside the E right-hand sides' quadrature
   int rhs_variant = 0;                        // 0: D5 (row factors); 2: V2 (whole patch only)
   double *el_eps = nullptr, *el_mu = nullptr;  // element material of the last adi_set_materials
@@ -512,6 +521,7 @@ struct SweepReq {
   double coef = 0.0;
   int64_t dims[3] = {0, 0, 0};   // box extents (x fastest); 0 = the whole N^3 patch
   const double* c = nullptr;     // modified: per-row c in the job's layout (nullptr: the patch's)
+  double* out2 = nullptr;        // derivative projection, TMA-staged kernel: out2 = out + coef M^{-1} A in
 };
 
 // tiles: legacy kernels flatten the fibers into tiles of tile_fibers; the TMA-staged kernel
@@ -539,6 +549,7 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_
     J.c = req[j].c ? req[j].c : P->c;
     J.iu = req[j].iu;
     J.base = req[j].base;
+    J.out2 = req[j].out2;
     J.coef = req[j].coef;
     J.axis = req[j].axis;
     active_range(P, req[j].comp, req[j].axis, J.lo, J.hi);
@@ -604,7 +615,7 @@ bool sweep_tma_maps(adi_patch P, const adi::SweepBatch& B, int mode, adi::SweepT
     const adi::SweepJob& J = B.job[j];
     if (mode == adi::SW_MOD && (!J.iu || !J.c)) return false;
     const double* aux = mode == adi::SW_MOD ? J.c : mode == adi::SW_DER ? J.base : J.in;
-    const double* piv = mode == adi::SW_MOD ? J.iu : J.in;
+    const double* piv = mode == adi::SW_MOD ? J.iu : (mode == adi::SW_DER && J.out2) ? J.out2 : J.in;
     if (!make_sweep_map(&maps.m[j][0], J.in, J.dims, J.axis) || !make_sweep_map(&maps.m[j][1], aux, J.dims, J.axis) ||
         !make_sweep_map(&maps.m[j][2], piv, J.dims, J.axis) || !make_sweep_map(&maps.m[j][3], J.out, J.dims, J.axis))
       return false;
@@ -660,6 +671,23 @@ bool launch_sweeps_res(adi_patch P, const SweepReq* req, int nreq, int mode, cud
 adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode, cudaStream_t st = nullptr,
                          double* ckpt = nullptr) {
   if (!st) st = P->stream;
+  bool two_out = false;
+  for (int j = 0; j < nreq; j++) two_out = two_out || req[j].out2 != nullptr;
+  if (two_out) {  // only the TMA-staged kernel writes a second output (hmerge_ok checks its conditions)
+    adi::SweepBatch B = make_batch(P, req, nreq, 32, 32);
+    if (ckpt) B.ckpt = ckpt;
+    adi::SweepTmaMaps maps;
+    if (mode != adi::SW_DER || !sweep_tma_maps(P, B, mode, maps))
+      return fail(ADI_ERR_STATE, "internal: two-output derivative projection without the TMA-staged kernel");
+    B.nck = (P->N + adi::ST_CH - 1) / adi::ST_CH;
+    LaunchScope ls(P, ADI_K_SWEEP_DER);
+    const int warps = adi::st_warps(mode);
+    const int64_t blocks_needed = ((int64_t)B.ntiles + warps - 1) / warps;
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks_needed, P->st_grid[mode]);
+    with_degree(P->p, [&](auto ops) { ops.sweep_tma(st, grid, B, maps, mode); });
+    CUDA_TRY(cudaGetLastError());
+    return ADI_OK;
+  }
   {
     adi_status rst = ADI_OK;
     if (launch_sweeps_res(P, req, nreq, mode, st, rst)) return rst;
@@ -945,10 +973,58 @@ adi_status rhs_e_v2(adi_patch P, int s, const double* const F[6], double* const 
   return ADI_OK;
 }
 
+// fused H projections possible on this patch now (uniform mu, TMA-staged derivative sweeps)?
+bool hmerge_ok(adi_patch P) {
+  if (!P->hmerge || P->slab || P->cfg.nranks != 1 || !P->Q[0]) return false;
+  if (!P->mu_uniform || P->h_general || P->overlap) return false;
+  if (!(P->use_st & (1 << adi::SW_DER)) || P->st_grid[adi::SW_DER] < 1 || !tma_encoder()) return false;
+  if (P->use_res || P->use_tw || (P->N & 1)) return false;
+  return true;
+}
+
+// Q = H + c1(s) D_{a1(s)} E_{x1(s)}: the first projection of substep s into Q (bootstrap of the
+// fused schedule, outside the step graph)
+adi_status q_bootstrap(adi_patch P) {
+  const double* E[3] = {P->F[0], P->F[1], P->F[2]};
+  const double* H[3] = {P->F[3], P->F[4], P->F[5]};
+  adi_status st = h_update_first(P, 1, H, E, P->Q);
+  if (!st) P->q_valid = true;
+  return st;
+}
+
 adi_status substep(adi_patch P, int s) {
   adi_status st;
   const double* E[3] = {P->F[0], P->F[1], P->F[2]};
   const double* H[3] = {P->F[3], P->F[4], P->F[5]};
+  if (hmerge_ok(P) && P->q_valid) {
+    if (P->rhs_variant == 2) {
+      if ((st = rhs_e_v2(P, s, P->F, P->R))) return st;
+    } else {
+      adi_status st3 = ADI_OK;
+      if (rhs_e3(P, s, P->F, P->R, 0, 0, 0, 0, st3)) {
+        if (st3) return st3;
+      } else {
+        for (int d = 0; d < 3; d++)
+          if ((st = rhs_e(P, s, d, E, H, P->R[d]))) return st;
+      }
+    }
+    if ((st = solve_e_range(P, s, 0, 3, P->R, P->R))) return st;
+    // H_new = Q + c2 D_{a2} En_{x2} (into G), Q <- H_new + c2 D_{a2} En_{x2} (the next substep's
+    // first projection: a1(next) = a2(s), x1(next) = x2(s), c1(next) = c2(s))
+    const double b = P->b_scalar;
+    SweepReq r[3];
+    for (int d = 0; d < 3; d++) {
+      const int a2 = s == 1 ? (d + 2) % 3 : (d + 1) % 3, x2 = s == 1 ? (d + 1) % 3 : (d + 2) % 3;
+      r[d] = SweepReq{3 + d, a2, P->R[x2], P->G[d], nullptr, P->Q[d], s == 1 ? b : -b};
+      r[d].out2 = P->Q[d];
+    }
+    if ((st = launch_sweeps(P, r, 3, adi::SW_DER))) return st;
+    for (int d = 0; d < 3; d++) {
+      std::swap(P->F[d], P->R[d]);
+      std::swap(P->F[3 + d], P->G[d]);
+    }
+    return ADI_OK;
+  }
   // uniform mu: the first H projection needs only the substep's starting fields, so it
   // runs as a concurrent graph branch (side stream, own checkpoints) beside the E path
   // -- the latency-bound sweeps leave issue slots and bandwidth to share.
@@ -1884,6 +1960,7 @@ adi_status factorize(adi_patch P) {
 // a uniform mu^ (then b is the scalar of the derivative-projection H update).
 adi_status derive_abc(adi_patch P, double* epsh, double* muh) {
   drop_graph(P);  // kernel parameters (b, band constants) change with tau / materials
+  P->q_valid = false;
   if (!P->slab) {
     adi::abc_kernel<<<148 * 8, 256, 0, P->stream>>>(epsh, muh, P->tau, P->U, P->a, P->b, P->c);
   } else {
@@ -1966,6 +2043,7 @@ void adi_destroy(adi_patch P) {
   f(P->cy), f(P->xbuf[0]), f(P->xbuf[1]);
   f(P->d_zsp[0]), f(P->d_zsp[1]), f(P->ztips), f(P->zgath);
   f(P->el_eps), f(P->el_mu), f(P->v2buf[0]), f(P->v2buf[1]), f(P->d_v2tab), f(P->d_v2start);
+  for (int i = 0; i < 3; i++) f(P->Q[i]);
   if (P->tr) {
     if (auto* L = dynamic_cast<LoopTransport*>(P->tr)) {
       std::lock_guard<std::mutex> lk(L->g->m);
@@ -2024,6 +2102,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_SW_TMA")) P->use_st = atoi(s);
   if (const char* s = getenv("ADI_SW_RES")) P->use_res = atoi(s);
   if (const char* s = getenv("ADI_RHS3")) P->use_rhs3 = atoi(s);
+  if (const char* s = getenv("ADI_HMERGE")) P->hmerge = atoi(s);
   if (adi_status st0 = sweep_setup(P)) return bail(st0);
   if (with_degree(p, [](auto ops) { return ops.rhs_attrs(); }) != cudaSuccess) return bail(fail(ADI_ERR_CUDA, "rhs kernel attributes: %s", cudaGetErrorString(cudaGetLastError())));
   if (P->use_rhs3 && p <= 3) {
@@ -2205,6 +2284,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
     if (!dmalloc(&P->F[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc fields (%zu doubles)", U));
   for (int i = 0; i < 3 && whole; i++)
     if (!dmalloc(&P->R[i], U) || !dmalloc(&P->G[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc scratch fields"));
+  for (int i = 0; i < 3 && whole && P->hmerge; i++)
+    if (!dmalloc(&P->Q[i], U)) return bail(fail(ADI_ERR_OOM, "cudaMalloc fused-projection buffers"));
   if (whole &&
       (!dmalloc(&P->a, U) || !dmalloc(&P->b, U) || !dmalloc(&P->c, U) || !dmalloc(&P->epsh, U) || !dmalloc(&P->muh, U)))
     return bail(fail(ADI_ERR_OOM, "cudaMalloc material arrays"));
@@ -2433,6 +2514,7 @@ adi_status adi_set_fields(adi_patch P, const double* const f[6]) {
   cudaError_t e = cudaStreamSynchronize(P->stream);
   if (e != cudaSuccess) return poison(P, fail(ADI_ERR_CUDA, "adi_set_fields: %s", cudaGetErrorString(e)));
   P->have_fields = true;
+  P->q_valid = false;
   return ADI_OK;
 }
 
@@ -2532,6 +2614,7 @@ adi_status adi_step(adi_patch P, int64_t k) {
     return fail(ADI_ERR_STATE, "adi_step: variant V2 needs element-wise materials (adi_set_materials)");
   if (k == 0) return ADI_OK;
   adi_status st = ADI_OK;
+  if (hmerge_ok(P) && !P->q_valid && (st = q_bootstrap(P))) return poison(P, st);
   if (P->timing || (P->slab && !P->tr->capturable())) {
     st = run_steps(P, k);
   } else {
@@ -2622,6 +2705,7 @@ adi_status adi_debug_materials_tf(adi_patch P, double* eps_tf, double* mu_tf) {
 }
 
 static adi_status stage_io_begin(adi_patch P, double** tmp, int ntmp) {
+  P->q_valid = false;  // debug stages may replace the fields
   for (int i = 0; i < ntmp; i++) {
     if (cudaMalloc(&tmp[i], P->U * sizeof(double)) != cudaSuccess) {
       cudaGetLastError();

@@ -89,6 +89,7 @@ struct SweepJob {
   const double* c;    // per-test-function c (MOD)
   const double* iu;   // cached pivots 1/u_kk of this family (MOD)
   const double* base; // DER: out = base + coef * M^{-1} A u
+  double* out2;       // DER, TMA-staged kernel only (or nullptr): out2 = out + coef * M^{-1} A u
   double coef;
   int axis;           // 0 = x, 1 = y, 2 = z
   int lo, hi;         // active rows along the axis (PEC, D1)

@@ -531,23 +531,34 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       bwd_chunk(std::false_type{}, sl, r0, y, us, ivs);
     }
     double* dst = sl;  // the solution overwrites the chunk's input rows (DER: its base rows)
+    double y2[DER ? CH : 1];
     if (DER) {
 #pragma unroll
       for (int q = 0; q < P; q++) hd[q] = (r0 + q < hi && r0 + q >= lo) ? at(sl, q) : 0.0;
       dst = sl + ST_ARR;
+      // out = base + coef x; with out2: also out2 = out + coef x (the next substep's first
+      // projection of the same derivative, SURVEY §8(a) note; same operations as two launches)
 #pragma unroll
-      for (int r = 0; r < CH; r++) y[r] = fma(coef, y[r], at(sl + ST_ARR, r));
+      for (int r = 0; r < CH; r++) {
+        const double x = y[r];
+        y[r] = fma(coef, x, at(sl + ST_ARR, r));
+        y2[r] = fma(coef, x, y[r]);
+      }
     }
     __syncwarp();  // every lane has read the slot
 #pragma unroll
     for (int r = 0; r < CH; r++)
-      if (r0 + r >= lo && r0 + r < hi) atw(dst, r) = y[r];  // rows outside [lo, hi) keep their loaded value
+      if (r0 + r >= lo && r0 + r < hi) {
+        atw(dst, r) = y[r];  // rows outside [lo, hi) keep their loaded value
+        if (DER && J.out2) atw(sl, r) = y2[r];  // the chunk's u rows are consumed (hd saved)
+      }
     st_fence_async();  // every lane's shared writes -> visible to the async (TMA) proxy
     __syncwarp();
     if (lane == 0) {
       int x, yy, z;
       coords(c, x, yy, z);
       st_store(m_out, x, yy, z, dst, pol_drop);
+      if (DER && J.out2) st_store(m_iu, x, yy, z, sl, pol_drop);
       st_commit();
       // refill the slot of chunk c+1 (stored one iteration ago) with chunk c+1-RS
       const int nxt_c = c + 1 - RS;

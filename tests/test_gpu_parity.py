@@ -697,3 +697,55 @@ def test_v2_contract():
     with pytest.raises(adi.AdiError) as e:  # per-test-function materials: no element material
         G.step(1)
     assert e.value.status == adi.ADI_ERR_STATE
+
+
+def _patch_env(env, n, p, tau):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return adi.Patch(n, p, tau)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,p", [(34, 2), (29, 3)])
+def test_fused_h_projections_bitwise(n, p):
+    """Fused H projections (one derivative-projection launch per substep writing H_new = Q + c x and
+    the next substep's Q' = H_new + c x): bit-identical to the two-launch schedule, across steps,
+    after set_fields / set_tau (Q re-bootstrapped), with a source and phantom material; fewer
+    launches per step."""
+    N = n + p
+    tau = 0.02
+    eps = workloads.element_eps(n, "phantom4")
+    f = workloads.random_fields(N, 95)
+    g = workloads.random_fields(N, 96)
+    sig = workloads.signal("modsine", tau, 20)
+    pos = workloads.dipole_position(n)
+    outs, lps = [], []
+    for hm in ("1", "0"):
+        G = _patch_env({"ADI_HMERGE": hm}, n, p, tau)
+        G.set_materials(eps)
+        G.set_point_source(2, pos, sig)
+        G.set_fields(f)
+        G.step(3)
+        a = G.get_fields()
+        G.step(2)
+        b = G.get_fields()
+        G.set_fields(g)
+        G.step(2)
+        c = G.get_fields()
+        G.set_tau(0.013)
+        G.step(2)
+        d = G.get_fields()
+        outs.append([a, b, c, d])
+        lps.append(G.launches_per_step)
+        G.close()
+    for x, y in zip(outs[0], outs[1]):
+        for c in range(6):
+            assert np.array_equal(x[c], y[c]), c
+    assert lps[0] < lps[1], lps
