@@ -297,9 +297,9 @@ def parallelism_label(args):
     if ws == 1:
         return "single GPU, whole patch, CUDA graph per step"
     return (f"z-slab decomposition over {ws} GPUs (one process per GPU), the library's distributed adi_step: "
-            "NCCL halo exchange before the RHS stencils; mass sweeps and derivative projections along z by the "
-            "partitioned (SPIKE) solve in place (2p interface values per fiber all-gathered, NEXT-1); batched "
-            "all-to-all z<->y transposes only around the row-modified z sweep; one CUDA graph per step")
+            "NCCL halo exchange before the RHS stencils; every z sweep by the partitioned (SPIKE) solve in "
+            "place (NEXT-1: 2p interface values per fiber all-gathered for the mass sweeps and derivative "
+            "projections, 2p + 4p^2 spike tips for the row-modified sweep), no transposes; one CUDA graph per step")
 
 
 def config_dict(cfg, args):
@@ -351,8 +351,8 @@ class _Whole:
 
 class _Dist:
     """N > 1 GPUs: this rank's z-slab patch; the library runs the distributed schedule itself
-    (adi_step over NCCL: halo exchanges, the partitioned z-solve of the constant sweeps, batched
-    z<->y transposes around the row-modified z sweep; one CUDA graph per step)."""
+    (adi_step over NCCL: halo exchanges and the partitioned z-solve of every z sweep; one CUDA
+    graph per step)."""
 
     def __init__(self, cfg, local, seed):
         import torch

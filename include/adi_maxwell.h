@@ -177,8 +177,9 @@ adi_status adi_set_rhs_variant(adi_patch patch, int32_t variant);
  *   1 (default): partitioned (SPIKE) solve in place on the z-slabs -- each rank solves its
  *      diagonal block of the banded matrix, the ranks all-gather 2p interface values per fiber
  *      (instead of the fiber), and every rank finishes with the precomputed rows of the
- *      2pR x 2pR interface system (adi_zsolve_tables); the row-modified z sweep (per-fiber
- *      matrix) keeps the transposes;
+ *      2pR x 2pR interface system (adi_zsolve_tables); the row-modified z sweep (a per-fiber
+ *      matrix M + diag(c) S) all-gathers 2p + 4p^2 spike tips per fiber and eliminates the
+ *      block-tridiagonal interface system per fiber: no transposes at all;
  *   0: every z sweep between all-to-all transposes (the per-fiber arithmetic of a whole patch:
  *      bit-identical for any number of ranks).
  * *active (may be NULL) = 1 if mode 1 is in effect: a distributed patch whose every rank holds

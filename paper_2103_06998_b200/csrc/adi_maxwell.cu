@@ -243,8 +243,9 @@ struct adi_patch_s {
   double* d_zsp[2] = {nullptr, nullptr};   // per variant: fac | tw | cb | q
   int zsp_g0l[2] = {0, 0}, zsp_m[2] = {0, 0};
   size_t zsp_off[2][4] = {};
-  double* ztips = nullptr;  // [3][2p][N^2]
-  double* zgath = nullptr;  // [R][3][2p][N^2]
+  double* ztips = nullptr;  // [max(3 * 2p, 2p + 4p^2)][N^2]
+  double* zgath = nullptr;  // [R][...]
+  double* zscr = nullptr;   // (p + 1) z-slabs: U rows of the row-modified segment solve
   // Fused H projections (uniform mu, whole patch): the second derivative projection of a substep
   // and the first one of the next substep apply the SAME operator to the SAME new E component
   // (axis a2(s) = a1(s+1), field x2(s) = x1(s+1), coefficient c2(s) = c1(s+1), both substeps and
@@ -1537,6 +1538,40 @@ adi_status zsolve_spike(adi_patch P, int mode, const SweepReq* zj, int nzj) {
   return ADI_OK;
 }
 
+// NEXT-1 for the row-modified z sweep (per-fiber matrix M + diag(c) S, spike.cuh): per-fiber spike
+// tips computed on the fly, one all-gather of 2p + 4p^2 values per fiber, the block-tridiagonal
+// interface system eliminated per fiber towards the rank's interfaces, the corrected segment solve.
+adi_status zsolve_spike_mod(adi_patch P, const SweepReq& j) {
+  const int p = P->p;
+  int lo, hi;
+  active_range(P, j.comp, 2, lo, hi);
+  const int v = lo == 0 ? 0 : 1;
+  if (!P->d_zsp[v]) return fail(ADI_ERR_STATE, "z-spike: no partition for the PEC range of component %d", j.comp);
+  adi::SpikeModArgs A{};
+  A.NN = (int64_t)P->N * P->N;
+  A.nz = P->nz, A.R = P->nrk, A.r = P->rank, A.N = P->N, A.k0 = P->k0;
+  A.g0l = P->zsp_g0l[v], A.m = P->zsp_m[v];
+  A.f = j.in;
+  A.c = P->c;
+  A.out = j.out;
+  A.scratch = P->zscr;
+  A.Mb = P->d_tab + (size_t)adi::OP_M * P->N * P->W;
+  A.Sb = P->d_tab + (size_t)adi::OP_S * P->N * P->W;
+  A.tips = P->ztips;
+  A.gath = P->zgath;
+  {
+    LaunchScope ls(P, ADI_K_SWEEP_MOD);
+    with_degree(p, [&](auto ops) { ops.spike_mod(P->stream, A, 0); });
+    CUDA_TRY(cudaGetLastError());
+  }
+  adi_status st = P->tr->allgather(P, P->ztips, P->zgath, (int64_t)(2 * p + 4 * p * p) * A.NN);
+  if (st) return st;
+  LaunchScope ls(P, ADI_K_SWEEP_MOD);
+  with_degree(p, [&](auto ops) { ops.spike_mod(P->stream, A, 1); });
+  CUDA_TRY(cudaGetLastError());
+  return ADI_OK;
+}
+
 // One stage of sweeps in slab mode: x / y jobs on the z-slabs, z jobs on y-slabs between one
 // batched z -> y transpose of their inputs (DER: u and base) and one y -> z transpose back.
 // Jobs carry INNER z-slab pointers of halo'd buffers (in, out, base).
@@ -1560,7 +1595,12 @@ adi_status dist_sweeps(adi_patch P, int mode, const SweepReq* jobs, int nj, cons
   adi_status st;
   if (nl && (st = launch_sweeps(P, loc, nl, mode))) return st;
   if (!nzj) return ADI_OK;
-  if (mode != adi::SW_MOD && P->zsolve == 1 && P->zspike_ok) return zsolve_spike(P, mode, zj, nzj);
+  if (P->zsolve == 1 && P->zspike_ok) {
+    if (mode != adi::SW_MOD) return zsolve_spike(P, mode, zj, nzj);
+    for (int q = 0; q < nzj; q++)
+      if ((st = zsolve_spike_mod(P, zj[q]))) return st;
+    return ADI_OK;
+  }
   // transpose in: inputs (and DER bases) -> Y
   double* src[3];
   double* dst[3];
@@ -2041,7 +2081,7 @@ void adi_destroy(adi_patch P) {
   for (int i = 0; i < 6; i++) f(P->iu[i]);
   for (int i = 0; i < 6; i++) f(P->Y[i]);
   f(P->cy), f(P->xbuf[0]), f(P->xbuf[1]);
-  f(P->d_zsp[0]), f(P->d_zsp[1]), f(P->ztips), f(P->zgath);
+  f(P->d_zsp[0]), f(P->d_zsp[1]), f(P->ztips), f(P->zgath), f(P->zscr);
   f(P->el_eps), f(P->el_mu), f(P->v2buf[0]), f(P->v2buf[1]), f(P->d_v2tab), f(P->d_v2start);
   for (int i = 0; i < 3; i++) f(P->Q[i]);
   if (P->tr) {
@@ -2272,8 +2312,8 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
         P->zsp_g0l[v] = T.g0 - P->k0, P->zsp_m[v] = T.m;
       }
       if (ok) {
-        const size_t per = (size_t)3 * 2 * p * N * N;
-        if (!dmalloc(&P->ztips, per) || !dmalloc(&P->zgath, per * P->nrk))
+        const size_t per = (size_t)std::max(3 * 2 * p, 2 * p + 4 * p * p) * N * N;
+        if (!dmalloc(&P->ztips, per) || !dmalloc(&P->zgath, per * P->nrk) || !dmalloc(&P->zscr, (size_t)(p + 1) * P->UL))
           return bail(fail(ADI_ERR_OOM, "cudaMalloc z-spike exchange buffers"));
       }
       P->zspike_ok = ok;

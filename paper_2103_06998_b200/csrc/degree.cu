@@ -35,6 +35,8 @@ template <>
 cudaError_t Ops<ADI_P>::sweep_res_attrs() { return cudaErrorNotSupported; }
 template <>
 void Ops<ADI_P>::spike(cudaStream_t, const SpikeBatch&, int) {}
+template <>
+void Ops<ADI_P>::spike_mod(cudaStream_t, const SpikeModArgs&, int) {}
 #else
 
 namespace {
@@ -192,6 +194,13 @@ void Ops<ADI_P>::spike(cudaStream_t st, const SpikeBatch& B, int solve) {
   const dim3 grid((unsigned)((B.NN + 255) / 256), (unsigned)B.njobs);
   if (solve) spike_solve_kernel<ADI_P><<<grid, 256, 0, st>>>(B);
   else spike_tips_kernel<ADI_P><<<grid, 256, 0, st>>>(B);
+}
+
+template <>
+void Ops<ADI_P>::spike_mod(cudaStream_t st, const SpikeModArgs& A, int solve) {
+  const unsigned grid = (unsigned)((A.NN + 127) / 128);
+  if (solve) spike_mod_solve_kernel<ADI_P><<<grid, 128, 0, st>>>(A);
+  else spike_mod_tips_kernel<ADI_P><<<grid, 128, 0, st>>>(A);
 }
 
 #endif  // ADI_STUB

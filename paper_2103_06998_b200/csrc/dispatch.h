@@ -47,6 +47,8 @@ struct Ops {
   // NEXT-1 partitioned z-solve (spike.cuh): solve = 0: tip pass, 1: corrected banded solve;
   // grid (fiber blocks of 256, jobs).
   static void spike(cudaStream_t st, const SpikeBatch& B, int solve);
+  // ... of the row-modified z sweep (per-fiber matrix): solve = 0 tips, 1 interface + segment solve
+  static void spike_mod(cudaStream_t st, const SpikeModArgs& A, int solve);
   // Pivot cache of one row-modified family (job 0 of B).
   static void factor(cudaStream_t st, unsigned grid, const SweepBatch& B, double* iu, unsigned long long* bad, double tol);
 };

@@ -334,6 +334,15 @@ class DistPatch:
         jobs_z: dicts with 'comp', 'in' (z-slab), 'out' (z-slab) [, 'iu', 'base', 'coef']."""
         if not jobs_z:
             return
+        if self.ztab is not None and mode == MOD:
+            # per-fiber matrix: tips of y, W and V from the rank's block, all-gathered, the interface
+            # system solved per fiber (NEXT-1 for the row-modified z sweep)
+            for j in jobs_z:
+                j["v"] = 1 if (self.bc == 0 and j["comp"] < 2) else 0
+                tips = self.B.spike_mod_tips(j, self.ztab[j["v"]], self.k0, self.c, self.R, self.rank)
+                self.B.spike_mod_solve(j, self.ztab[j["v"]], self.k0, self.c, self.R, self.rank,
+                                       self.comm.allgather(tips))
+            return
         if self.ztab is not None and mode != MOD:
             if mode == DER:  # A u along z reads p planes beyond the slab
                 self.comm.halo_exchange([j["in_h"] for j in jobs_z])

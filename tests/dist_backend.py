@@ -190,3 +190,64 @@ class CpuBoxBackend:
                 out[g0l:g0l + m] = x
             out[:g0l] = 0.0
             out[g0l + m:] = 0.0
+
+    # -- NEXT-1 for the row-modified z sweep (restated from spike.cuh with dense per-fiber blocks) ---
+    def _mod_blocks(self, T, k0, c, R, r):
+        """Per fiber: A_r (m x m), C_r (p x p), B_r (p x p) of M + diag(c) S on the rank's block."""
+        g0, m, P = T["g0"], T["m"], self.p
+        g1 = g0 + m
+        cl = c.numpy().reshape(c.shape[0], -1)[g0 - k0:g1 - k0].T  # (nf, m): c of the block rows
+        M, S = self.M, self.S
+        A = M[g0:g1, g0:g1][None] + cl[:, :, None] * S[g0:g1, g0:g1][None]
+        C = np.zeros((cl.shape[0], P, P))
+        B = np.zeros((cl.shape[0], P, P))
+        if r > 0:
+            C = M[g0:g0 + P, g0 - P:g0][None] + cl[:, :P, None] * S[g0:g0 + P, g0 - P:g0][None]
+        if r < R - 1:
+            B = M[g1 - P:g1, g1:g1 + P][None] + cl[:, m - P:, None] * S[g1 - P:g1, g1:g1 + P][None]
+        return A, C, B
+
+    def spike_mod_tips(self, j, T, k0, c, R, r):
+        P, m, g0l = self.p, T["m"], T["g0"] - k0
+        A, C, B = self._mod_blocks(T, k0, c, R, r)
+        w = j["in"].numpy().reshape(j["in"].shape[0], -1)[g0l:g0l + m].T  # (nf, m)
+        X = np.zeros((A.shape[0], m, 1 + 2 * P))
+        X[:, :, 0] = w
+        X[:, :P, 1:1 + P] = C
+        X[:, m - P:, 1 + P:] = B
+        Y = np.linalg.solve(A, X)
+        tips = np.concatenate([Y[:, :P, 0], Y[:, m - P:, 0], Y[:, :P, 1:1 + P].reshape(-1, P * P),
+                               Y[:, m - P:, 1:1 + P].reshape(-1, P * P), Y[:, :P, 1 + P:].reshape(-1, P * P),
+                               Y[:, m - P:, 1 + P:].reshape(-1, P * P)], axis=1)
+        return torch.from_numpy(np.ascontiguousarray(tips.T))  # [2P + 4P^2, nf]
+
+    def spike_mod_solve(self, j, T, k0, c, R, r, gath):
+        P, m, g0l = self.p, T["m"], T["g0"] - k0
+        A, C, B = self._mod_blocks(T, k0, c, R, r)
+        G = gath.numpy()  # [R, 2P + 4P^2, nf]
+        nf = G.shape[2]
+        nK = 2 * P * R
+        K = np.tile(np.eye(nK), (nf, 1, 1))
+        rhs = np.zeros((nf, nK))
+        for s in range(R):
+            t = G[s].T  # (nf, 2P + 4P^2)
+            yt, yb = t[:, :P], t[:, P:2 * P]
+            Wt, Wb, Vt, Vb = (t[:, 2 * P + q * P * P:2 * P + (q + 1) * P * P].reshape(nf, P, P) for q in range(4))
+            rhs[:, 2 * P * s:2 * P * s + P] = yt
+            rhs[:, 2 * P * s + P:2 * P * (s + 1)] = yb
+            for rows, Vx, Wx in ((slice(2 * P * s, 2 * P * s + P), Vt, Wt), (slice(2 * P * s + P, 2 * P * (s + 1)), Vb, Wb)):
+                if s + 1 < R:
+                    K[:, rows, 2 * P * (s + 1):2 * P * (s + 1) + P] += Vx
+                if s > 0:
+                    K[:, rows, 2 * P * (s - 1) + P:2 * P * s] += Wx
+        xi = np.linalg.solve(K, rhs[:, :, None])[:, :, 0]
+        tn = xi[:, 2 * P * (r + 1):2 * P * (r + 1) + P] if r + 1 < R else np.zeros((nf, P))
+        bp = xi[:, 2 * P * (r - 1) + P:2 * P * r] if r > 0 else np.zeros((nf, P))
+        out = j["out"].numpy().reshape(j["out"].shape[0], -1)
+        w = j["in"].numpy().reshape(j["in"].shape[0], -1)[g0l:g0l + m].T.copy()
+        w[:, :P] -= np.einsum("fij,fj->fi", C, bp)
+        w[:, m - P:] -= np.einsum("fij,fj->fi", B, tn)
+        x = np.linalg.solve(A, w[:, :, None])[:, :, 0]
+        out[g0l:g0l + m] = x.T
+        out[:g0l] = 0.0
+        out[g0l + m:] = 0.0
