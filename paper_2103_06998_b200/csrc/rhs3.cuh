@@ -301,6 +301,9 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
                     double o0 = 0.0, o1 = 0.0;
 #pragma unroll
                     for (int q = 0; q < W; q++) {
+                      // interior A / B rows are antisymmetric stencils with an exact zero centre
+                      // (adi_create makes the interior exactly Toeplitz): skip that tap
+                      if (decltype(kx)::value && xop != OP_M && q == P) continue;
                       const double c0 = decltype(kx)::value ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u) * W + q];
                       const double c1 =
                           decltype(kx)::value ? args.kint[xop][q] : cxs[(xop * RX_TX + 2 * u + 1) * W + q];
@@ -352,6 +355,7 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
               if (FAST || yint) {
 #pragma unroll
                 for (int q = 0; q < W; q++) {
+                  if (yop != OP_M && q == P) continue;  // zero centre of the interior A / B rows
                   vA = fma(args.kint[yop][q], col[q], vA);
                   vB = fma(args.kint[yop][q], col[q + 1], vB);
                 }
