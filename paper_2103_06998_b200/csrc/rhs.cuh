@@ -61,9 +61,12 @@ constexpr int RX_TX = 32;
 constexpr int RX_TY = 16;
 constexpr int RX_THREADS = 256;  // 32 x 8, two output rows each
 constexpr int RX_MAXT = 4;
-constexpr int RX_RING = 3;
+#ifndef ADI_RX_RING
+#define ADI_RX_RING 2
+#endif
+constexpr int RX_RING = ADI_RX_RING;  // TMA ring slots (input planes in flight)
 #ifndef ADI_RX_KCMAX
-#define ADI_RX_KCMAX 64
+#define ADI_RX_KCMAX 128
 #endif
 constexpr int RX_KCMAX = ADI_RX_KCMAX;  // max z-chunk (rows of the per-block z-coefficient table)
 
@@ -251,9 +254,7 @@ __device__ __forceinline__ void rhs_tile(const RhsMaps& maps, const RhsArgs& arg
       rx_commit();  // (empty groups keep the wait arithmetic uniform)
     }
   };
-  produce(kbeg);
-  produce(kbeg + 1);
-  produce(kbeg + 2);
+  for (int q = 0; q < RX_RING; q++) produce(kbeg + q);
 
   double w[NT][2][W];
 #pragma unroll

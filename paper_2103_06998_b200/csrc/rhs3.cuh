@@ -210,9 +210,7 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
       for (int f = 0; f < 6; f++) tma_load_3d(slot + f * PLANEP, &maps.m[f], i0 - P, j0 - P, kin, &bar[st]);
     }
   };
-  produce(kbeg);
-  produce(kbeg + 1);
-  produce(kbeg + 2);
+  for (int q = 0; q < RX_RING; q++) produce(kbeg + q);
 
   // accumulators of the 2P+1 pending output planes: acc[group][plane slot][row]
   double acc[9][W][2];
