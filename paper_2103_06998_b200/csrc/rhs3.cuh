@@ -324,55 +324,58 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
         // Z[k][2P - jj] (row k of the band table); interior planes: the Toeplitz row
         const int kout0 = kin - P - zoff;  // output-local plane of jj = 0
         const bool zint = kg0 + kout0 >= 2 * P && kg0 + kout0 + 2 * P < N - 2 * P;
-        // z coefficients of this input plane, once per plane for the three z-operators M, A, B
-        // (the products below index them with compile-time operator and plane slot)
-        double zc[3][W];
-        if (zint) {
+        // z coefficients of this input plane for the three z-operators M, A, B: interior planes take
+        // the Toeplitz rows from the parameter bank (compile-time slots; the exact-zero centre of A / B
+        // skipped), boundary planes a per-plane register copy of the block's table
+        auto yz = [&](auto zi) {
+          constexpr bool ZI = decltype(zi)::value;
+          double zc[3][W];
+          if (!ZI) {
 #pragma unroll
-          for (int o = 0; o < 3; o++)
+            for (int jj = 0; jj < W; jj++) {
+              const int ko = min(max(kout0 + jj, k0), k1 - 1) - k0;
 #pragma unroll
-            for (int jj = 0; jj < W; jj++) zc[o][jj] = args.kint[o][2 * P - jj];
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < W; jj++) {
-            const int ko = min(max(kout0 + jj, k0), k1 - 1) - k0;
-#pragma unroll
-            for (int o = 0; o < 3; o++) zc[o][jj] = czs[(o * RX_KCMAX + ko) * W + 2 * P - jj];
-          }
-        }
-        rx3_static_for<0, NXS>([&](auto xsc) {
-          constexpr int xs = decltype(xsc)::value;
-          double col[W + 1];
-#pragma unroll
-          for (int q = 0; q <= W; q++) col[q] = sx[(xs * HY + 2 * ty + q) * RX_TX + tx];
-          rx3_static_for<0, Prog::NP>([&](auto tc) {
-            constexpr int t = decltype(tc)::value;
-            if constexpr (Prog::xslot(t) == xs) {
-              constexpr int yop = Prog::op(t, 1), zop = Prog::op(t, 2), g = Prog::gi(t);
-              double vA = 0.0, vB = 0.0;
-              if (FAST || yint) {
-#pragma unroll
-                for (int q = 0; q < W; q++) {
-                  if (yop != OP_M && q == P) continue;  // zero centre of the interior A / B rows
-                  vA = fma(args.kint[yop][q], col[q], vA);
-                  vB = fma(args.kint[yop][q], col[q + 1], vB);
-                }
-              } else {
-#pragma unroll
-                for (int q = 0; q < W; q++) {
-                  vA = fma(cys[(yop * RX_TY + 2 * ty) * W + q], col[q], vA);
-                  vB = fma(cys[(yop * RX_TY + 2 * ty + 1) * W + q], col[q + 1], vB);
-                }
-              }
-              if constexpr (Prog::sign(t) < 0.0) vA = -vA, vB = -vB;
-#pragma unroll
-              for (int jj = 0; jj < W; jj++) {
-                acc[g][jj][0] = fma(zc[zop][jj], vA, acc[g][jj][0]);
-                acc[g][jj][1] = fma(zc[zop][jj], vB, acc[g][jj][1]);
-              }
+              for (int o = 0; o < 3; o++) zc[o][jj] = czs[(o * RX_KCMAX + ko) * W + 2 * P - jj];
             }
+          }
+          rx3_static_for<0, NXS>([&](auto xsc) {
+            constexpr int xs = decltype(xsc)::value;
+            double col[W + 1];
+#pragma unroll
+            for (int q = 0; q <= W; q++) col[q] = sx[(xs * HY + 2 * ty + q) * RX_TX + tx];
+            rx3_static_for<0, Prog::NP>([&](auto tc) {
+              constexpr int t = decltype(tc)::value;
+              if constexpr (Prog::xslot(t) == xs) {
+                constexpr int yop = Prog::op(t, 1), zop = Prog::op(t, 2), g = Prog::gi(t);
+                double vA = 0.0, vB = 0.0;
+                if (FAST || yint) {
+#pragma unroll
+                  for (int q = 0; q < W; q++) {
+                    if (yop != OP_M && q == P) continue;  // zero centre of the interior A / B rows
+                    vA = fma(args.kint[yop][q], col[q], vA);
+                    vB = fma(args.kint[yop][q], col[q + 1], vB);
+                  }
+                } else {
+#pragma unroll
+                  for (int q = 0; q < W; q++) {
+                    vA = fma(cys[(yop * RX_TY + 2 * ty) * W + q], col[q], vA);
+                    vB = fma(cys[(yop * RX_TY + 2 * ty + 1) * W + q], col[q + 1], vB);
+                  }
+                }
+                if constexpr (Prog::sign(t) < 0.0) vA = -vA, vB = -vB;
+#pragma unroll
+                for (int jj = 0; jj < W; jj++) {
+                  if (ZI && zop != OP_M && jj == P) continue;
+                  const double z = ZI ? args.kint[zop][2 * P - jj] : zc[zop][jj];
+                  acc[g][jj][0] = fma(z, vA, acc[g][jj][0]);
+                  acc[g][jj][1] = fma(z, vB, acc[g][jj][1]);
+                }
+              }
+            });
           });
-        });
+        };
+        if (zint) yz(std::true_type{});
+        else yz(std::false_type{});
         if (NSX == 1) __syncthreads();  // sx consumed (two buffers: the next x-pass writes the other)
         // ---- output plane k = kin - P is complete
         {
