@@ -281,7 +281,10 @@ __device__ __forceinline__ void rhs3_tile(const Rhs3Maps& maps, const Rhs3Args& 
             constexpr int f = decltype(fc)::value;
 #pragma unroll
             for (int m = 0; m < 2; m++) {
-              const int ex = (tid - 40 * f + 4 * RX_THREADS) % RX_THREADS;
+              // the HY - 16 extra rows of field f go to whole warps (2 per field for P = 2), the warp
+              // pair rotating with f: no divergent partial warps (measured 1 % faster than a 40-thread
+              // rotation that splits warps)
+              const int ex = (tid - 64 * f + 8 * RX_THREADS) % RX_THREADS;
               const int yy = m == 0 ? xrow0 : 16 + (ex >> 4);
               if (m == 0 || ex < (HY - 16) * 16) {
                 const double2* rp = reinterpret_cast<const double2*>(slot + f * PLANEP + yy * HX + 2 * u);
