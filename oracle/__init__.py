@@ -5,8 +5,8 @@ TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 package.  The product path (``paper_2103_06998_b200``) never imports it and
 shares no code with it.
 
-The arithmetic lives in ``adi_oracle.c`` (plain C, fp64, single thread,
-``-O2 -ffp-contract=off``); this module is ctypes marshalling only.
+The arithmetic lives in ``adi_oracle.c`` (plain C, fp64, single thread unless
+``Patch.set_threads`` asks for more, ``-O2 -ffp-contract=off``); this module is ctypes marshalling only.
 Every function of the C file cites the PAPER.md passage it follows.
 """
 from __future__ import annotations
@@ -30,7 +30,7 @@ _dp = C.POINTER(C.c_double)
 def build(force: bool = False) -> str:
     """Compile liboracle.so in-tree (gcc, plain C)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-fPIC", "-shared", "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"]
         subprocess.run(cmd, check=True)
         os.replace(_LIB + ".tmp", _LIB)
     return _LIB
@@ -60,6 +60,7 @@ def lib():
             L.orc_point_load.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, _dp]
             L.orc_set_source.argtypes = [C.c_void_p, C.c_void_p, _dp, C.c_int64]
             L.orc_set_rhs_variant.argtypes = [C.c_void_p, C.c_int]
+            L.orc_set_threads.argtypes = [C.c_void_p, C.c_int]
             _lib = L
         return _lib
 
@@ -179,6 +180,11 @@ class Patch:
 
     def set_order_variant(self, v: int):
         self._L.orc_set_order_variant(self.h, int(v))
+
+    def set_threads(self, t: int):
+        """Split the independent-output loops (kron3 output points, sweep fibers) over t OpenMP
+        threads; results are bit-identical to the default single thread."""
+        self._L.orc_set_threads(self.h, int(t))
 
     def set_rhs_variant(self, v: int):
         """0: material of the test function on the RHS rows (D5); 2: element-wise material inside

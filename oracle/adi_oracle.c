@@ -1,7 +1,7 @@
 /*
  * oracle/adi_oracle.c -- TEST INFRASTRUCTURE ONLY.
  *
- * A plain, slow, single-threaded fp64 CPU implementation of the ADI
+ * A plain, slow fp64 CPU implementation of the ADI
  * isogeometric Maxwell time step of arXiv 2103.06998 ("PAPER.md" below,
  * cited as P:<line>).  It exists to define "correct" for the CUDA path in
  * paper_2103_06998_b200/ and is pinned by tests/ against values the paper
@@ -21,6 +21,13 @@
  * Layout (D14): coefficient (i,j,k) -> i + N*(j + N*k), x fastest.
  * Element (a,b,c) -> a + n*(b + n*c).
  * Components: 0..2 = E1,E2,E3 ; 3..5 = H1,H2,H3.
+ *
+ * Threads: single-threaded unless orc_set_threads(P, t > 1) is called (only
+ * tools/make_golden.py does, for the long c4 run).  Then the loops over
+ * independent outputs -- the output points of kron3 and the fibers of a
+ * sweep -- are split over t OpenMP threads; every output is still computed by
+ * exactly the same sequence of operations, so results are bit-identical to the
+ * single-threaded run (tests/test_oracle_pins.py::test_threads_bit_identical).
  */
 #include <math.h>
 #include <stdint.h>
@@ -55,7 +62,10 @@ typedef struct {
                         material inside the RHS quadrature (V2) */
   double *eps_el, *mu_el; /* element-wise material of the last orc_set_materials (NULL after _tf) */
   double max_growth; /* max growth factor seen in banded LU (pin P9) */
+  int threads;       /* OpenMP threads for the independent-output loops (<= 1: single thread) */
 } orc_patch;
+
+static int nthreads(const orc_patch* P) { return P->threads > 1 ? P->threads : 1; }
 
 #define IDX(N, i, j, k) ((int64_t)(i) + (int64_t)(N) * ((int64_t)(j) + (int64_t)(N) * (int64_t)(k)))
 
@@ -223,6 +233,7 @@ orc_patch* orc_create(int n, int p, double tau, int bc) {
 
 int orc_dims(orc_patch* P, int* N) { *N = P->N; return ORC_OK; }
 void orc_set_order_variant(orc_patch* P, int v) { P->order_variant = v; }
+void orc_set_threads(orc_patch* P, int t) { P->threads = t; }
 double orc_max_growth(orc_patch* P) { return P->max_growth; }
 int64_t orc_step_index(orc_patch* P) { return P->step_index; }
 
@@ -424,6 +435,7 @@ static double ent(const double* X, int tr, int N, int r, int l) { return tr ? X[
 static void kron3(const orc_patch* P, const double* X, int xT, const double* Y, int yT, const double* Z, int zT,
                   const double* u, double* out) {
   int N = P->N, p = P->p;
+#pragma omp parallel for num_threads(nthreads(P)) schedule(static)
   for (int t = 0; t < N; t++)
     for (int s = 0; s < N; s++)
       for (int r = 0; r < N; r++) {
@@ -503,15 +515,21 @@ static int sweep(orc_patch* P, int comp, int axis, const double* c, double* u) {
   int lo1, hi1, lo2, hi2;
   active_range(P, comp, ax1, &lo1, &hi1);
   active_range(P, comp, ax2, &lo2, &hi2);
-  double* W = (double*)malloc(sizeof(double) * m * (3 * p + 1));
-  double* f = (double*)malloc(sizeof(double) * m);
-  double* x = (double*)malloc(sizeof(double) * m);
-  int status = ORC_OK;
-  for (int q2 = lo2; q2 < hi2 && status == ORC_OK; q2++)
-    for (int q1 = lo1; q1 < hi1 && status == ORC_OK; q1++) {
+  int64_t nf1 = hi1 - lo1, nfib = nf1 * (hi2 - lo2);
+  int64_t bad_fiber = nfib; /* first singular fiber in (q2, q1) loop order */
+  int bad_row = 0;
+  double gmax = P->max_growth;
+#pragma omp parallel num_threads(nthreads(P))
+  {
+    double* W = (double*)malloc(sizeof(double) * m * (3 * p + 1));
+    double* f = (double*)malloc(sizeof(double) * m);
+    double* x = (double*)malloc(sizeof(double) * m);
+    double gloc = 0.0;
+#pragma omp for schedule(static)
+    for (int64_t q = 0; q < nfib; q++) {
       int ijk[3];
-      ijk[ax1] = q1;
-      ijk[ax2] = q2;
+      ijk[ax1] = lo1 + (int)(q % nf1);
+      ijk[ax2] = lo2 + (int)(q / nf1);
       memset(W, 0, sizeof(double) * m * (3 * p + 1));
       for (int k = lo; k < hi; k++) {
         ijk[axis] = k;
@@ -524,19 +542,28 @@ static int sweep(orc_patch* P, int comp, int axis, const double* c, double* u) {
       double g = 0.0;
       int bad = band_solve_pp(m, p, W, f, x, &g);
       if (bad) {
-        snprintf(g_err, sizeof g_err, "sweep: singular pivot (comp %d, axis %d, fiber (%d,%d), row %d)", comp, axis, q1, q2, lo + bad - 1);
-        status = ORC_ERR_SINGULAR;
-        break;
+#pragma omp critical(orc_sweep_bad)
+        if (q < bad_fiber) { bad_fiber = q; bad_row = lo + bad - 1; }
+        continue;
       }
-      if (g > P->max_growth) P->max_growth = g;
+      if (g > gloc) gloc = g;
       for (int k = lo; k < hi; k++) {
         ijk[axis] = k;
         u[IDX(N, ijk[0], ijk[1], ijk[2])] = x[k - lo];
       }
     }
-  free(W); free(f); free(x);
-  if (status == ORC_OK) zero_inactive(P, comp, u); /* rows outside the active set stay 0 */
-  return status;
+#pragma omp critical(orc_sweep_growth)
+    if (gloc > gmax) gmax = gloc;
+    free(W); free(f); free(x);
+  }
+  P->max_growth = gmax;
+  if (bad_fiber < nfib) {
+    snprintf(g_err, sizeof g_err, "sweep: singular pivot (comp %d, axis %d, fiber (%d,%d), row %d)", comp, axis,
+             lo1 + (int)(bad_fiber % nf1), lo2 + (int)(bad_fiber / nf1), bad_row);
+    return ORC_ERR_SINGULAR;
+  }
+  zero_inactive(P, comp, u); /* rows outside the active set stay 0 */
+  return ORC_OK;
 }
 
 /* Stiffened axis of E component d (0-based) in substep s (1 or 2):

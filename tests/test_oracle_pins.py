@@ -933,3 +933,26 @@ def test_oracle_errors_and_states():
         P.set_materials(np.concatenate([np.ones(26), [-1.0]]))
     with pytest.raises(oracle.OracleError):
         P.set_materials_tf(np.full(P.U, np.nan))
+
+
+@pytest.mark.parametrize("p,bc", [(2, 0), (3, 1)])
+def test_threads_bit_identical(p, bc):
+    """orc_set_threads only splits independent outputs (kron3 points, sweep fibers) over OpenMP
+    threads: the fields after two steps with a source equal the single-threaded run bit for bit."""
+    n, tau = 7, 0.05
+    N = n + p
+    eps = workloads.element_eps(n, "phantom5")
+    f = workloads.random_fields(N, 11)
+    sig = np.sin(np.arange(4) * 0.3)
+    out = []
+    for t in (1, 4):
+        P = oracle.Patch(n, p, tau, bc)
+        P.set_threads(t)
+        P.set_materials(eps)
+        P.set_fields(f)
+        P.set_source([None, P.point_load(0.3, 0.6, 0.45), None], sig)
+        P.step(2)
+        out.append(P.get_fields())
+    for x, y in zip(*out):
+        assert np.array_equal(x, y)
+

@@ -72,6 +72,7 @@ def sample_indices(x: np.ndarray, seed: int) -> np.ndarray:
 
 CKPT = os.path.join(ROOT, "build", "golden_ckpt")
 CHUNK = 25
+THREADS = int(os.environ.get("ORC_THREADS", os.cpu_count() or 1))
 
 
 def _patch(I, fields, m0):
@@ -79,6 +80,7 @@ def _patch(I, fields, m0):
     (the oracle reads signal[step_index], step_index counting from 0 on a fresh patch), so resuming
     performs exactly the arithmetic of an uninterrupted run."""
     P = oracle.Patch(I["n"], I["p"], I["tau"])
+    P.set_threads(THREADS)  # bit-identical to one thread (oracle header; test_threads_bit_identical)
     P.set_materials(I["eps"])
     P.set_fields(fields)
     if I["source"] is not None:
