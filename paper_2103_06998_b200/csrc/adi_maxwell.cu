@@ -193,6 +193,10 @@ struct adi_patch_s {
   double tw_vb[2][25] = {}, tw_wt[2][25] = {}, tw_kk[2][25] = {};
   int sw_grid_tw[3] = {0, 0, 0};       // persistent grid of the twisted mass / - / derivative sweep
   int use_tw = 0;                      // ADI_SW_TWISTED=1 enables the twisted (two-segment SPIKE) sweeps
+  // twisted row-modified sweep (sweep_twm.cuh), ADI_SW_TWM: 0 never, 1 always, 2 (default) when the
+  // launch has fewer than 8 tiles of 32 fibers per resident warp -- measured at c4 (128^3, 1.3 tiles
+  // per warp): 0.082 vs 0.088 ms per launch; at c5 (21 tiles per warp) 3.74 vs 3.68 ms
+  int use_twm = 2;
   std::vector<double> kfac[2];
   std::vector<double> kM, kS;          // interior Toeplitz rows of M, S
   int sw_grid[3] = {0, 0, 0};          // persistent grid of the mass / modified / derivative sweep
@@ -580,7 +584,21 @@ adi::SweepBatch make_batch(adi_patch P, const SweepReq* req, int nreq, int tile_
 
 // twisted (two-segment SPIKE) launch possible for these jobs?
 bool twisted(adi_patch P, const SweepReq* req, int nreq, int mode) {
-  if (!P->use_tw || mode == adi::SW_MOD) return false;
+  if (mode == adi::SW_MOD) {  // twisted factorisation: both segments need P rows for the interface
+    if (!P->use_twm) return false;
+    int64_t tiles = 0;
+    for (int j = 0; j < nreq; j++) {
+      int lo, hi;
+      active_range(P, req[j].comp, req[j].axis, lo, hi);
+      if ((hi - lo) / 2 < P->p) return false;
+      const int ax = req[j].axis;
+      int64_t d[3];
+      for (int a = 0; a < 3; a++) d[a] = req[j].dims[a] ? req[j].dims[a] : P->N;
+      tiles += (d[(ax + 1) % 3] * d[(ax + 2) % 3] + 31) / 32;
+    }
+    return P->use_twm == 1 || tiles < 8 * (int64_t)P->sw_grid[adi::SW_MOD] * adi::SW_WARPS;
+  }
+  if (!P->use_tw) return false;
   for (int j = 0; j < nreq; j++) {
     int lo, hi;
     active_range(P, req[j].comp, req[j].axis, lo, hi);
@@ -724,7 +742,7 @@ adi_status launch_sweeps(adi_patch P, const SweepReq* req, int nreq, int mode, c
 adi_status sweep_setup(adi_patch P) {
   int occ[3] = {0, 0, 0}, occ_tw[3] = {0, 0, 0};
   cudaError_t e = with_degree(P->p, [&](auto ops) { return ops.sweep_attrs(occ, occ_tw); });
-  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1 || occ[2] < 1 || occ_tw[0] < 1 || occ_tw[2] < 1) {
+  if (e != cudaSuccess || occ[0] < 1 || occ[1] < 1 || occ[2] < 1 || occ_tw[0] < 1 || occ_tw[1] < 1 || occ_tw[2] < 1) {
     cudaGetLastError();
     return fail(ADI_ERR_CUDA, "sweep kernel attributes: %s", cudaGetErrorString(e));
   }
@@ -2138,6 +2156,7 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
   if (const char* s = getenv("ADI_SW_BPS_DER")) P->sw_bps[2] = atoi(s);
   if (const char* s = getenv("ADI_H_GENERAL")) P->h_general = atoi(s);
   if (const char* s = getenv("ADI_SW_TWISTED")) P->use_tw = atoi(s);
+  if (const char* s = getenv("ADI_SW_TWM")) P->use_twm = atoi(s);
   if (const char* s = getenv("ADI_OVERLAP")) P->overlap = atoi(s);
   if (const char* s = getenv("ADI_SW_TMA")) P->use_st = atoi(s);
   if (const char* s = getenv("ADI_SW_RES")) P->use_res = atoi(s);

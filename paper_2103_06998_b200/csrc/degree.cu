@@ -113,7 +113,8 @@ cudaError_t Ops<ADI_P>::rhs3_attrs() {
 template <>
 void Ops<ADI_P>::sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode, bool twisted) {
   const unsigned block = 32 * SW_WARPS;
-  if (twisted && mode == SW_DER) sweep_tw_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
+  if (twisted && mode == SW_MOD) sweep_twm_kernel<ADI_P><<<grid, block, sw_smem_bytes<SW_MOD>(), st>>>(B);
+  else if (twisted && mode == SW_DER) sweep_tw_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
   else if (twisted) sweep_tw_kernel<ADI_P, SW_MASS><<<grid, block, sw_smem_bytes<SW_MASS>(), st>>>(B);
   else if (mode == SW_MOD) sweep_kernel<ADI_P, SW_MOD><<<grid, block, sw_smem_bytes<SW_MOD>(), st>>>(B);
   else if (mode == SW_DER) sweep_kernel<ADI_P, SW_DER><<<grid, block, sw_smem_bytes<SW_DER>(), st>>>(B);
@@ -136,7 +137,7 @@ cudaError_t Ops<ADI_P>::sweep_attrs(int occ[3], int occ_tw[3]) {
   if ((e = attr_occ(sweep_kernel<ADI_P, SW_MOD>, sw_smem_bytes<SW_MOD>(), &occ[SW_MOD]))) return e;
   if ((e = attr_occ(sweep_kernel<ADI_P, SW_DER>, sw_smem_bytes<SW_DER>(), &occ[SW_DER]))) return e;
   if ((e = attr_occ(sweep_tw_kernel<ADI_P, SW_MASS>, sw_smem_bytes<SW_MASS>(), &occ_tw[SW_MASS]))) return e;
-  occ_tw[SW_MOD] = occ[SW_MOD];
+  if ((e = attr_occ(sweep_twm_kernel<ADI_P>, sw_smem_bytes<SW_MOD>(), &occ_tw[SW_MOD]))) return e;
   return attr_occ(sweep_tw_kernel<ADI_P, SW_DER>, sw_smem_bytes<SW_DER>(), &occ_tw[SW_DER]);
 }
 

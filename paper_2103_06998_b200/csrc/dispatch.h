@@ -11,6 +11,7 @@
 #include "rhs3.cuh"
 #include "sweep.cuh"
 #include "sweep_tw.cuh"
+#include "sweep_twm.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_res.cuh"
 #include "spike.cuh"
@@ -29,7 +30,8 @@ struct Ops {
   static void rhs3(cudaStream_t st, dim3 grid, const Rhs3Args& args, const Rhs3Maps& maps, int s);
   static cudaError_t rhs3_attrs();
   // One batched sweep launch (persistent grid chosen by the caller).
-  // twisted: two-segment SPIKE variant (mass / derivative modes, sweep_tw.cuh).
+  // twisted: two-segment variant (mass / derivative modes: SPIKE, sweep_tw.cuh;
+  // row-modified mode: twisted factorisation, sweep_twm.cuh).
   static void sweep(cudaStream_t st, unsigned grid, const SweepBatch& B, int mode, bool twisted);
   // Set the dynamic shared memory of the sweep kernels; occ[mode] / occ_tw[mode] =
   // resident blocks per SM (SweepMode order: mass, modified, derivative projection).

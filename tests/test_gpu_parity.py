@@ -749,3 +749,39 @@ def test_fused_h_projections_bitwise(n, p):
         for c in range(6):
             assert np.array_equal(x[c], y[c]), c
     assert lps[0] < lps[1], lps
+
+
+@pytest.mark.parametrize("n,p", [(2, 1), (2, 2), (6, 1), (13, 2), (7, 3), (35, 2), (64, 2), (67, 3), (30, 4), (21, 5)])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_sweep_mod_twisted(n, p, bc):
+    """The twisted row-modified sweep (sweep_twm.cuh: top segment top-down, bottom segment
+    bottom-up on the mirrored stencil, 2p x 2p interface solve) against the oracle's pivoted
+    banded LU, and against the one-lane-per-fiber kernel (ADI_SW_TWM=0), for every axis, both
+    PEC variants (bc 0) and the natural full range (bc 1); odd and even active lengths, segments
+    of one to five 8-row chunks, Toeplitz-fast and boundary chunks, and patches too short to
+    split (fallback)."""
+    N = n + p
+    eps = workloads.random_tf(N, 21 + n, 1.0, 80.0)
+    O = oracle.Patch(n, p, 0.05, bc)
+    O.set_materials_tf(eps)
+    G = {}
+    for k in ("1", "0"):
+        with _env(ADI_SW_TWM=k):
+            G[k] = adi.Patch(n, p, 0.05, bc)
+        G[k].set_materials_tf(eps)
+    rng = np.random.default_rng(7 * n + p)
+    for axis in (0, 1, 2):
+        for comp in (0, 1, 2):
+            rhs = rng.uniform(-1, 1, N ** 3)
+            if bc == 0:  # zero outside the PEC active set (D1)
+                u = rhs.reshape(N, N, N)
+                for ax in range(3):
+                    if ax != comp:
+                        sl = [slice(None)] * 3
+                        sl[2 - ax] = [0, N - 1]
+                        u[tuple(sl)] = 0.0
+            ref = O.sweep(comp, axis, True, rhs)
+            tw = G["1"].sweep(comp, axis, True, rhs)
+            one = G["0"].sweep(comp, axis, True, rhs)
+            assert rel(tw, ref) <= 1e-12, (axis, comp, rel(tw, ref))
+            assert rel(tw, one) <= 1e-12, (axis, comp)
