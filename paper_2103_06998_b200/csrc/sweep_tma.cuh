@@ -199,6 +199,11 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
 #pragma unroll
     for (int q = 0; q < W; q++) kf[q] = var ? B.kfac[1][q] : B.kfac[0][q];
   }
+#ifdef ADI_ST_PRESCALE
+  double ks[P];  // U entries scaled by the inverse pivot: back substitution with one FMA on the chain
+#pragma unroll
+  for (int q = 0; q < P; q++) ks[q] = MOD ? 0.0 : kf[P + 1 + q] * kf[P];
+#endif
   double yw[P];
   double uw[MOD ? P : 1][P];
   double iw[MOD ? P : 1];
@@ -427,10 +432,17 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
     for (int q = 0; q < P; q++) xv[CH + q] = xw[q];
 #pragma unroll
     for (int r = CH - 1; r >= 0; r--) {
+#ifdef ADI_ST_PRESCALE
+      double x = yv[P + r] * kf[P];
+#pragma unroll
+      for (int q = P - 1; q >= 0; q--) x = fma(-ks[q], xv[r + 1 + q], x);
+      xv[r] = x;
+#else
       double x = yv[P + r];
 #pragma unroll
       for (int q = P - 1; q >= 0; q--) x = fma(-kf[P + 1 + q], xv[r + 1 + q], x);
       xv[r] = x * kf[P];
+#endif
     }
 #pragma unroll
     for (int q = 0; q < P; q++) xw[q] = xv[q];
