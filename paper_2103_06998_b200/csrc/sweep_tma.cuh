@@ -170,10 +170,10 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
   auto atw = [&](double* a, int r) -> double& {
     return xax ? a[lane * 16 + ((((r >> 1) ^ (lane & 7)) << 1) | (r & 1))] : a[r * 32 + lane];
   };
-  // lane 0: load chunk c (na arrays) into slot c % RS
-  auto issue = [&](int c, int na, uint64_t pol) {
+  // lane 0: load chunk c (na arrays) into slot s (= c % RS, tracked incrementally by the callers:
+  // the per-chunk modulo and the per-row range predicates were half of the issue slots at c5)
+  auto issue = [&](int c, int s, int na, uint64_t pol) {
     if (lane == 0) {
-      const int s = c % RS;
       double* sl = ring + s * SLOT;
       int x, y, z;
       coords(c, x, y, z);
@@ -183,11 +183,12 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       if (na > 2) st_load(sl + 2 * ST_ARR, m_iu, x, y, z, &bar[s], pol);
     }
   };
-  auto wait_slot = [&](int c) {
-    const int s = c % RS;
+  auto wait_slot = [&](int s) {
     mbar_wait(&bar[s], (phase >> s) & 1u);
     phase ^= 1u << s;
   };
+  auto next_slot = [](int s) { return s + 1 == RS ? 0 : s + 1; };
+  auto prev_slot = [](int s) { return s == 0 ? RS - 1 : s - 1; };
 
   const double* fac = var ? B.fac[1] : B.fac[0];
   const double* Mb = var ? B.Mb[1] : B.Mb[0];
@@ -327,10 +328,16 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       for (int q = 0; q < P; q++) dv[q] = (r0 - P + q >= lo) ? pv[P - 1 - q] : 0.0;
     }
   };
-  auto chunk_fast = [&](int r0) {
-    return r0 >= lo && r0 + CH <= hi && (MOD || DER ? (r0 >= 2 * P && r0 + CH <= N - 2 * P) : true) &&
-           (MOD ? true : (r0 >= hk && r0 + CH <= tk));
-  };
+  // chunks [cf0, cf1) are "fast": every row active, interior stencils / converged factors
+  int cf0, cf1;
+  {
+    int a = lo, b = hi;
+    if (MOD || DER) a = max(a, 2 * P), b = min(b, N - 2 * P);
+    if (!MOD) a = max(a, hk), b = min(b, tk);
+    cf0 = (a + CH - 1) / CH;
+    cf1 = b / CH;
+  }
+  auto chunk_fast = [&](int c) { return c >= cf0 && c < cf1; };
   // (DER) u at row r0+r of chunk slot sl; rows past the chunk from nx (next chunk) or hd (saved head)
   auto der_u = [&](const double* sl, const double* nxs, const double* hd, int r0, int r) -> double {
     if (r0 + r >= hi || r0 + r < lo) return 0.0;
@@ -454,32 +461,38 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
   constexpr int AHEAD = DER ? 1 : 0;
   const int pre = min(RS, nc);
   constexpr int NA1 = DER ? 1 : NA;  // arrays loaded in pass 1 (DER: u only; base in pass 2)
-  for (int c = 0; c < pre; c++) issue(c, NA1, pol_keep);
-  int waited = 0;  // chunks [0, waited) have completed
-  for (int c = 0; c < nc; c++) {
-    const int need = min(c + AHEAD, nc - 1);
-    while (waited <= need) wait_slot(waited++);
-    const double* sl = ring + (c % RS) * SLOT;
-    const double* nxs = (DER && c + 1 < nc) ? ring + ((c + 1) % RS) * SLOT : nullptr;
+  for (int c = 0; c < pre; c++) issue(c, c, NA1, pol_keep);
+  // chunk c is waited for in order; DER also needs chunk c + 1 (AHEAD) before eliminating chunk c
+  for (int c = 0, sc = 0; c < nc; c++, sc = next_slot(sc)) {
+    const int sn = next_slot(sc);
+    if (AHEAD) {
+      if (c == 0) wait_slot(sc);
+      if (c + 1 < nc) wait_slot(sn);
+    } else {
+      wait_slot(sc);
+    }
+    const double* sl = ring + sc * SLOT;
+    const double* nxs = (DER && c + 1 < nc) ? ring + sn * SLOT : nullptr;
     const int r0 = c * CH;
+    const bool fastc = chunk_fast(c);
     if (DER) der_prime(sl, r0);
     save_state(c);
-    if (!MOD && chunk_fast(r0)) {
+    if (!MOD && fastc) {
       double yv[P + CH];
       fwd_fast_cm(sl, nxs, nullptr, yv);
-    } else if (chunk_fast(r0)) {
+    } else if (fastc) {
       fwd_chunk(std::true_type{}, sl, nxs, nullptr, r0, nullptr, nullptr, nullptr);
     } else {
       fwd_chunk(std::false_type{}, sl, nxs, nullptr, r0, nullptr, nullptr, nullptr);
     }
     __syncwarp();
-    if (c + RS < nc) issue(c + RS, NA1, pol_keep);
+    if (c + RS < nc) issue(c + RS, sc, NA1, pol_keep);
   }
   // ---------------- pass 2: recompute per chunk, back substitution ----------
   // MASS/MOD keep the last min(RS, nc) chunks of pass 1; DER reloads every chunk (u and base).
   const int keep_from = DER ? nc : nc - pre;  // chunks >= keep_from are still resident
   if (DER) {
-    for (int c = nc - 1; c >= max(0, nc - (RS - 1)); c--) issue(c, NA, pol_drop);
+    for (int c = nc - 1; c >= max(0, nc - (RS - 1)); c--) issue(c, c % RS, NA, pol_drop);
   }
 #pragma unroll
   for (int q = 0; q < P; q++) xw[q] = 0.0;
@@ -519,21 +532,22 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
     }
   };
   load_prev(nc - 1);
-  for (int c = nc - 1; c >= 0; c--) {
-    if (c < keep_from) wait_slot(c);
-    double* sl = ring + (c % RS) * SLOT;
+  for (int c = nc - 1, sc = (nc - 1) % RS; c >= 0; c--, sc = prev_slot(sc)) {
+    if (c < keep_from) wait_slot(sc);
+    double* sl = ring + sc * SLOT;
     const int r0 = c * CH;
+    const bool fastc = chunk_fast(c);
     set_state(nxt, pv, pc, r0);
     if (c > 0) load_prev(c - 1);
     if (DER) der_prime(sl, r0);
     double y[CH];
     double us[CH * UW];
     double ivs[MOD ? CH : 1];
-    if (!MOD && chunk_fast(r0)) {
+    if (!MOD && fastc) {
       double yv[P + CH];
       fwd_fast_cm(sl, nullptr, hd, yv);
       bwd_fast_cm(yv, y);
-    } else if (chunk_fast(r0)) {
+    } else if (fastc) {
       fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us, ivs);
       bwd_chunk(std::true_type{}, sl, r0, y, us, ivs);
     } else {
@@ -558,12 +572,21 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       }
     }
     __syncwarp();  // every lane has read the slot
+    if (fastc) {  // every row active: plain stores at constant offsets
 #pragma unroll
-    for (int r = 0; r < CH; r++)
-      if (r0 + r >= lo && r0 + r < hi) {
-        atw(dst, r) = y[r];  // rows outside [lo, hi) keep their loaded value
-        if (DER && J.out2) atw(sl, r) = y2[r];  // the chunk's u rows are consumed (hd saved)
+      for (int r = 0; r < CH; r++) atw(dst, r) = y[r];
+      if (DER && J.out2) {
+#pragma unroll
+        for (int r = 0; r < CH; r++) atw(sl, r) = y2[r];
       }
+    } else {
+#pragma unroll
+      for (int r = 0; r < CH; r++)
+        if (r0 + r >= lo && r0 + r < hi) {
+          atw(dst, r) = y[r];  // rows outside [lo, hi) keep their loaded value
+          if (DER && J.out2) atw(sl, r) = y2[r];  // the chunk's u rows are consumed (hd saved)
+        }
+    }
     st_fence_async();  // every lane's shared writes -> visible to the async (TMA) proxy
     __syncwarp();
     if (lane == 0) {
@@ -576,7 +599,7 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       const int nxt_c = c + 1 - RS;
       if (nxt_c >= 0 && nxt_c < keep_from) {
         st_wait_read<1>();
-        issue(nxt_c, NA, pol_drop);
+        issue(nxt_c, next_slot(sc), NA, pol_drop);
       }
     }
     __syncwarp();
