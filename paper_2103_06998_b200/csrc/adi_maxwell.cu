@@ -2242,6 +2242,10 @@ adi_status adi_create(const adi_config* cfg, adi_patch* out) {
       P->tk[var] = t;
       P->kfac[var].assign(11, 0.0);
       for (int q = 0; q < W; q++) P->kfac[var][q] = fac[(size_t)mid * W + q];
+      // the table holds the reference row itself in [h, t): an unpredicated table read (the TMA
+      // sweep's medium chunks) then equals the kernels' "in ? kfac : table" select bit for bit
+      for (int k = h; k < t; k++)
+        for (int q = 0; q < W; q++) fac[(size_t)k * W + q] = fac[(size_t)mid * W + q];
     }
     band_from_dense(P->M, false, N, p, lo, hi, Mb.data());
     band_from_dense(P->S, false, N, p, lo, hi, Sb.data());

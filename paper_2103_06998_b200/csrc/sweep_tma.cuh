@@ -36,6 +36,7 @@
 
 namespace adi {
 
+using st_med = std::integral_constant<int, 2>;  // chunk tag: every row active, per-row tables
 constexpr int ST_CH = 16;              // rows per chunk (x sweeps: one 128-byte swizzle row per fiber)
 constexpr int ST_ARR = 32 * ST_CH;     // doubles per array per slot (4 KB)
 #ifndef ADI_ST_WARPS_MASS
@@ -233,9 +234,14 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       return fma(cc, sq, mq);
     }
   };
+  // fast tag: true_type = interior chunk (constants), st_med = every row active but table factors /
+  // boundary stencils (unpredicated table reads: the host stores the reference row in rows [hk, tk),
+  // so the read equals the select of the general path bit for bit), false_type = general
   auto fac_entry = [&](auto fast, int row, int q) -> double {
-    if constexpr (decltype(fast)::value) {
+    if constexpr (decltype(fast)::value == 1) {
       return kf[q];
+    } else if constexpr (decltype(fast)::value == 2) {
+      return __ldg(fac + (size_t)row * W + q);
     } else {
       const bool in = row >= hk && row < tk;
       return in ? kf[q] : __ldg(fac + (size_t)row * W + q);
@@ -246,9 +252,9 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
 #pragma unroll
     for (int q = 0; q < W; q++) {
       double aq;
-      if constexpr (decltype(fast)::value) {
+      if constexpr (decltype(fast)::value == 1) {
         aq = B.kA[q];
-      } else {
+      } else {  // (general and medium chunks: the A table is shared with the RHS kernels, keep the select)
         const bool in = row >= 2 * P && row < N - 2 * P;
         aq = in ? B.kA[q] : __ldg(B.Ab + (size_t)row * W + q);
       }
@@ -338,6 +344,9 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
     cf1 = b / CH;
   }
   auto chunk_fast = [&](int c) { return c >= cf0 && c < cf1; };
+  // (MASS / DER) chunks [cm0, cm1) have every row active: outside [cf0, cf1) they take the medium path
+  const int cm0 = (lo + CH - 1) / CH, cm1 = hi / CH;
+  auto chunk_med = [&](int c) { return !MOD && c >= cm0 && c < cm1; };
   // (DER) u at row r0+r of chunk slot sl; rows past the chunk from nx (next chunk) or hd (saved head)
   auto der_u = [&](const double* sl, const double* nxs, const double* hd, int r0, int r) -> double {
     if (r0 + r >= hi || r0 + r < lo) return 0.0;
@@ -482,6 +491,8 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       fwd_fast_cm(sl, nxs, nullptr, yv);
     } else if (fastc) {
       fwd_chunk(std::true_type{}, sl, nxs, nullptr, r0, nullptr, nullptr, nullptr);
+    } else if (chunk_med(c)) {
+      fwd_chunk(st_med{}, sl, nxs, nullptr, r0, nullptr, nullptr, nullptr);
     } else {
       fwd_chunk(std::false_type{}, sl, nxs, nullptr, r0, nullptr, nullptr, nullptr);
     }
@@ -536,7 +547,7 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
     if (c < keep_from) wait_slot(sc);
     double* sl = ring + sc * SLOT;
     const int r0 = c * CH;
-    const bool fastc = chunk_fast(c);
+    const bool fastc = chunk_fast(c), medc = !fastc && chunk_med(c);
     set_state(nxt, pv, pc, r0);
     if (c > 0) load_prev(c - 1);
     if (DER) der_prime(sl, r0);
@@ -550,6 +561,9 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
     } else if (fastc) {
       fwd_chunk(std::true_type{}, sl, nullptr, hd, r0, y, us, ivs);
       bwd_chunk(std::true_type{}, sl, r0, y, us, ivs);
+    } else if (medc) {
+      fwd_chunk(st_med{}, sl, nullptr, hd, r0, y, us, ivs);
+      bwd_chunk(st_med{}, sl, r0, y, us, ivs);
     } else {
 #pragma unroll
       for (int r = 0; r < CH; r++) y[r] = 0.0;
@@ -572,7 +586,7 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
       }
     }
     __syncwarp();  // every lane has read the slot
-    if (fastc) {  // every row active: plain stores at constant offsets
+    if (fastc || medc) {  // every row active: plain stores at constant offsets
 #pragma unroll
       for (int r = 0; r < CH; r++) atw(dst, r) = y[r];
       if (DER && J.out2) {
