@@ -346,7 +346,10 @@ __device__ __forceinline__ void st_tile(const SweepBatch& B, const SweepTmaMaps&
   auto chunk_fast = [&](int c) { return c >= cf0 && c < cf1; };
   // (MASS / DER) chunks [cm0, cm1) have every row active: outside [cf0, cf1) they take the medium path
   const int cm0 = (lo + CH - 1) / CH, cm1 = hi / CH;
-  auto chunk_med = [&](int c) { return !MOD && c >= cm0 && c < cm1; };
+#ifndef ADI_ST_MED_DER
+#define ADI_ST_MED_DER 0  // the derivative projection is traffic bound: the medium path only costs it registers
+#endif
+  auto chunk_med = [&](int c) { return (MODE == SW_MASS || (DER && ADI_ST_MED_DER)) && c >= cm0 && c < cm1; };
   // (DER) u at row r0+r of chunk slot sl; rows past the chunk from nx (next chunk) or hd (saved head)
   auto der_u = [&](const double* sl, const double* nxs, const double* hd, int r0, int r) -> double {
     if (r0 + r >= hi || r0 + r < lo) return 0.0;
