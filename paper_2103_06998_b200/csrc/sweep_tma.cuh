@@ -78,9 +78,26 @@ struct SweepTmaMaps {
   CUtensorMap m[SW_MAXJOBS][4];
 };
 
+// fraction of the pass-1 lines that get evict_last priority, per mode: where the in-flight window of
+// all resident warps exceeds L2 (derivative projection at 8 warps per SM: 156 MB), protecting every
+// line protects none; a fraction that fits stays resident for the pass-2 re-read
+#ifndef ADI_ST_KEEP_DER
+#define ADI_ST_KEEP_DER 0.15  // measured at c5: 1.0 3.49 ms, 0.7 3.46, 0.5 3.44, 0.3 3.42, 0.15 3.39 per launch
+#endif
+#ifndef ADI_ST_KEEP_MASS
+#define ADI_ST_KEEP_MASS 1.0
+#endif
+#define ADI_ST_STR2(x) #x
+#define ADI_ST_STR(x) ADI_ST_STR2(x)
+template <int MODE>
 __device__ __forceinline__ uint64_t st_policy_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  if (MODE == SW_DER)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " ADI_ST_STR(ADI_ST_KEEP_DER) ";\n" : "=l"(p));
+  else if (MODE == SW_MASS)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " ADI_ST_STR(ADI_ST_KEEP_MASS) ";\n" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t st_policy_first() {
@@ -645,7 +662,7 @@ sweep_tma_kernel(const __grid_constant__ SweepBatch B, const __grid_constant__ S
   }
   __syncwarp();
   unsigned phase = 0;  // bit s: parity of the next completion of slot s
-  const uint64_t pol_keep = st_policy_last(), pol_drop = st_policy_first();
+  const uint64_t pol_keep = st_policy_last<MODE>(), pol_drop = st_policy_first();
   const int gw = blockIdx.x * WARPS + wib;
   const int nw = gridDim.x * WARPS;
   double* ck = B.ckpt + (size_t)gw * B.nck * SWD * 32 + lane;
